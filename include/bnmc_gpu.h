@@ -1,0 +1,166 @@
+/* bnmc_gpu.h — C-ABI of the B200-native order-MCMC hot path.
+ *
+ * Drop-in boundary for the reference's hot path (arXiv:1210.5128 order-space
+ * MCMC, reference project "bnmc", paths relative to /root/reference/proj):
+ *
+ *   reference interface                                   replaced by
+ *   ---------------------------------------------------   ----------------------------------
+ *   ScoreCache::build(const Dataset&, const RunConfig&)   bnmc_gpu_table_build
+ *     (include/bnmc/scoring.hpp:126, src/scoring.cpp:162-192)
+ *   count_statistics(const Dataset&, int, ParentSet)      bnmc_gpu_count_statistics
+ *     (include/bnmc/scoring.hpp:79, src/scoring.cpp:82-109)
+ *   ScoreCache::estimate_bytes (scoring.hpp:123)          bnmc_gpu_table_estimate_bytes
+ *   ScoreCache::load / prebuilt cache (scoring.hpp:153,   bnmc_gpu_table_upload
+ *     sampler.hpp:63-65 `prebuilt`)
+ *   ScoreCache::save / at / lookup (scoring.hpp:141-152)  bnmc_gpu_table_download
+ *   OrderScorer::OrderScorer(cache, priors, EngineConfig) bnmc_gpu_table_set_priors
+ *     (include/bnmc/engine.hpp:77-78; PpfTable scoring.hpp:96-112)
+ *   OrderScorer::score(const Order&) (engine.hpp:80,      bnmc_gpu_score_order(s)
+ *     src/engine.cpp:60-98); score_order (scoring.cpp:261-289)
+ *   run_mcmc(data, cfg, priors, prebuilt)                 bnmc_gpu_run_chains
+ *     (include/bnmc/sampler.hpp:63-65, src/sampler.cpp:58-116)
+ *
+ * Conventions:
+ *   * Every function returns a status: 0 ok, 2 usage (reference UsageError),
+ *     3 data (DataError), 4 capacity (CapacityError), 5 CUDA, 1 other. The
+ *     message of the last failure on the calling thread is returned by
+ *     bnmc_gpu_last_error_message().
+ *   * The caller owns every host buffer; the library owns device memory through
+ *     the opaque handle. Calls are synchronous at return. One handle must not be
+ *     used from two threads at once.
+ *   * There is no CPU fallback: without a usable sm_100 device every compute
+ *     entry point fails with status 5.
+ *   * Layouts: datasets are row-major uint8 m x n (Dataset::cells, types.hpp:77-79);
+ *     prior matrices are row-major double n x n with r[child*n + parent]
+ *     (PriorMatrix, types.hpp:149-163), NULL = neutral; tables are double
+ *     n x S(n-1,s) in (node, global index) order — the BNSC body order
+ *     (scoring.hpp:148-153, scoring.cpp:194-238); parent sets are u64 node masks.
+ */
+#ifndef BNMC_GPU_H
+#define BNMC_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  BNMC_OK = 0,
+  BNMC_ERR = 1,
+  BNMC_USAGE = 2,
+  BNMC_DATA = 3,
+  BNMC_CAPACITY = 4,
+  BNMC_CUDA = 5
+};
+
+enum { BNMC_ALPHA_BDEU = 0, BNMC_ALPHA_K2 = 1 };
+
+typedef struct bnmc_table bnmc_table;
+
+/* The scoring fields of RunConfig (types.hpp:167-183) that the table depends on. */
+typedef struct {
+  int max_parents;           /* s, RunConfig::max_parents, in [0,8] */
+  double gamma;              /* per-parent penalty, (0,1] */
+  double ess;                /* equivalent sample size, > 0 */
+  int alpha_mode;            /* BNMC_ALPHA_BDEU | BNMC_ALPHA_K2 */
+  uint64_t memory_cap_bytes; /* RunConfig::memory_cap_bytes (checked like estimate_bytes) */
+  int device;                /* CUDA ordinal this table lives on */
+} bnmc_score_params;
+
+const char* bnmc_gpu_last_error_message(void);
+/* Library/ABI version, e.g. 10000 for 1.0.0. */
+int bnmc_gpu_version(void);
+/* Number of usable sm_100 devices (0 when none; status 5 when the runtime fails). */
+int bnmc_gpu_device_count(int* out);
+
+/* S(n-1,s) * 8: ScoreCache::estimate_bytes (scoring.cpp:157-160). */
+uint64_t bnmc_gpu_table_estimate_bytes(int n, int s);
+/* S(c,s) = sum_{j<=s} C(c,j): bounded_subset_count (combinatorics.hpp:32-36). */
+uint64_t bnmc_gpu_bounded_subset_count(int c, int s);
+
+/* ScoreCache::build on the device: joint-state count tables + BD local scores
+ * for every (node, parent set |pi|<=s), then the PPF fold for prior_r.
+ * Bit-exact with the reference's canonical build. */
+int bnmc_gpu_table_build(const uint8_t* cells, const int* cards, uint64_t m, int n,
+                         const bnmc_score_params* params, const double* prior_r,
+                         bnmc_table** out);
+
+/* Node-row-sharded build (multi-GPU precompute): allocate the full
+ * table but compute only rows [row_begin, row_end). The caller exchanges rows
+ * (e.g. an NCCL all-gather over the buffer from bnmc_gpu_table_rows_buffer)
+ * and then calls bnmc_gpu_table_finalize. */
+int bnmc_gpu_table_build_rows(const uint8_t* cells, const int* cards, uint64_t m, int n,
+                              const bnmc_score_params* params, const double* prior_r,
+                              int row_begin, int row_end, bnmc_table** out);
+/* Device pointer and byte size of the fp64 local-score rows (n x S doubles,
+ * contiguous, row stride S). Valid until bnmc_gpu_table_free. */
+int bnmc_gpu_table_rows_buffer(bnmc_table* t, void** dev_ptr, uint64_t* bytes,
+                               uint64_t* row_stride_elems);
+/* Rebuild the derived scan table after rows were written externally. */
+int bnmc_gpu_table_finalize(bnmc_table* t);
+
+/* Prebuilt cache: host table in BNSC body order (e.g. from ScoreCache::load). */
+int bnmc_gpu_table_upload(const double* table, int n, const bnmc_score_params* params,
+                          const double* prior_r, bnmc_table** out);
+/* Replace the pairwise prior (re-folds the PPF into the scan table). */
+int bnmc_gpu_table_set_priors(bnmc_table* t, const double* prior_r);
+int bnmc_gpu_table_info(const bnmc_table* t, int* n, int* s, uint64_t* entries_per_node);
+/* Local scores (no PPF) back to the host in BNSC body order: n * S doubles. */
+int bnmc_gpu_table_download(const bnmc_table* t, double* out);
+/* Device-side timings of the last build: count+score kernel and PPF fold, ms. */
+int bnmc_gpu_table_build_ms(const bnmc_table* t, float* count_score_ms, float* fold_ms);
+int bnmc_gpu_table_free(bnmc_table* t);
+
+/* count_statistics for `count` (node, pset) pairs on the device (same kernel
+ * code as the build). out receives, for entry e, r_e * cards[node_e] u32 cells
+ * at out + offsets[e] (offsets computed by the caller as the prefix sum of
+ * r_e * card, configs_out[e] = r_e). */
+int bnmc_gpu_count_statistics(const uint8_t* cells, const int* cards, uint64_t m, int n,
+                              int count, const int* nodes, const uint64_t* psets,
+                              const uint64_t* offsets, uint32_t* out,
+                              uint64_t* configs_out, int device);
+
+/* OrderScorer::score for `count` orders (perms: count x n positions->node).
+ * Outputs per order: parent masks (n, indexed by node), per-node effective
+ * best (n, by node) and the total summed in ascending node order. Any output
+ * pointer may be NULL. Bit-exact with the reference (tie rule included). */
+int bnmc_gpu_score_orders(bnmc_table* t, const int* perms, int count, uint64_t* masks_out,
+                          double* best_out, double* totals_out);
+int bnmc_gpu_score_order(bnmc_table* t, const int* perm, uint64_t* masks_out,
+                         double* best_out, double* total_out);
+
+/* run_mcmc parameters (RunConfig fields of the sampler). */
+typedef struct {
+  uint64_t iterations; /* >= 1 */
+  int track_top;       /* BestGraphTracker capacity, >= 1 */
+  int strict;          /* RunConfig::strict_paper_tracker */
+  int scan_mode;       /* 0 = auto; 1 = fp32 keys + exact fp64 resolve; 2 = fp64 */
+  int reserved;
+} bnmc_chain_params;
+
+/* Run n_chains independent chains, chain c seeded with seeds[c] exactly as
+ * run_mcmc(data, cfg{seed=seeds[c]}, priors, prebuilt=table), in lockstep on
+ * the device (CUDA-Graph / persistent loop, no per-iteration host round trip).
+ * Host outputs (any may be NULL), chain-major:
+ *   trace_proposed[c*iters + t], trace_accepted[..], trace_best[..]  (TraceRow)
+ *   final_order[c*n + p], final_score[c], accepted[c]
+ *   tracker_count[c], tracker_masks[(c*K + e)*n + node], tracker_totals[c*K + e]
+ * device_ms (optional) receives the device time of the sampling loop. */
+int bnmc_gpu_run_chains(bnmc_table* t, const uint64_t* seeds, int n_chains,
+                        const bnmc_chain_params* params, double* trace_proposed,
+                        uint8_t* trace_accepted, double* trace_best, int* final_order,
+                        double* final_score, uint64_t* accepted, int* tracker_count,
+                        uint64_t* tracker_masks, double* tracker_totals, float* device_ms);
+
+/* Scan statistics of the last run_chains call: node-row rescans performed
+ * (summed over chains and iterations), distinct rows streamed (after batching
+ * chains), and the device time of the scan kernel alone (ms). */
+int bnmc_gpu_last_scan_stats(const bnmc_table* t, uint64_t* row_rescans,
+                             uint64_t* rows_streamed, float* scan_ms, uint64_t* scan_launches);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

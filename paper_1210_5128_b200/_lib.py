@@ -1,0 +1,135 @@
+"""ctypes binding of the product C-ABI (include/bnmc_gpu.h, include/bnmc_synth.h).
+
+Loads the in-tree ``paper_1210_5128_b200/libbnmc_b200.so`` (built by
+``__graft_entry__.build()`` / ``make -C paper_1210_5128_b200/csrc``). There is no
+fallback: if the library is missing, or no sm_100 device is visible when a
+compute entry point is called, the call raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libbnmc_b200.so")
+
+_u8p = np.ctypeslib.ndpointer(np.uint8, flags="C_CONTIGUOUS")
+_i32p = np.ctypeslib.ndpointer(np.int32, flags="C_CONTIGUOUS")
+_u32p = np.ctypeslib.ndpointer(np.uint32, flags="C_CONTIGUOUS")
+_u64p = np.ctypeslib.ndpointer(np.uint64, flags="C_CONTIGUOUS")
+_f64p = np.ctypeslib.ndpointer(np.float64, flags="C_CONTIGUOUS")
+_vp = C.c_void_p
+
+
+class ScoreParams(C.Structure):
+    _fields_ = [("max_parents", C.c_int), ("gamma", C.c_double), ("ess", C.c_double),
+                ("alpha_mode", C.c_int), ("memory_cap_bytes", C.c_uint64), ("device", C.c_int)]
+
+
+class ChainParams(C.Structure):
+    _fields_ = [("iterations", C.c_uint64), ("track_top", C.c_int), ("strict", C.c_int),
+                ("scan_mode", C.c_int), ("reserved", C.c_int)]
+
+
+# Every exported symbol with its ctypes signature: (restype, argtypes).
+SIGNATURES = {
+    "bnmc_gpu_last_error_message": (C.c_char_p, []),
+    "bnmc_gpu_version": (C.c_int, []),
+    "bnmc_gpu_device_count": (C.c_int, [C.POINTER(C.c_int)]),
+    "bnmc_gpu_table_estimate_bytes": (C.c_uint64, [C.c_int, C.c_int]),
+    "bnmc_gpu_bounded_subset_count": (C.c_uint64, [C.c_int, C.c_int]),
+    "bnmc_gpu_table_build": (C.c_int, [_u8p, _i32p, C.c_uint64, C.c_int, C.POINTER(ScoreParams),
+                                       _vp, C.POINTER(_vp)]),
+    "bnmc_gpu_table_build_rows": (C.c_int, [_u8p, _i32p, C.c_uint64, C.c_int,
+                                            C.POINTER(ScoreParams), _vp, C.c_int, C.c_int,
+                                            C.POINTER(_vp)]),
+    "bnmc_gpu_table_rows_buffer": (C.c_int, [_vp, C.POINTER(_vp), C.POINTER(C.c_uint64),
+                                             C.POINTER(C.c_uint64)]),
+    "bnmc_gpu_table_finalize": (C.c_int, [_vp]),
+    "bnmc_gpu_table_upload": (C.c_int, [_f64p, C.c_int, C.POINTER(ScoreParams), _vp,
+                                        C.POINTER(_vp)]),
+    "bnmc_gpu_table_set_priors": (C.c_int, [_vp, _vp]),
+    "bnmc_gpu_table_info": (C.c_int, [_vp, C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                      C.POINTER(C.c_uint64)]),
+    "bnmc_gpu_table_download": (C.c_int, [_vp, _f64p]),
+    "bnmc_gpu_table_build_ms": (C.c_int, [_vp, C.POINTER(C.c_float), C.POINTER(C.c_float)]),
+    "bnmc_gpu_table_free": (C.c_int, [_vp]),
+    "bnmc_gpu_count_statistics": (C.c_int, [_u8p, _i32p, C.c_uint64, C.c_int, C.c_int, _i32p,
+                                            _u64p, _u64p, _u32p, _u64p, C.c_int]),
+    "bnmc_gpu_score_orders": (C.c_int, [_vp, _i32p, C.c_int, _vp, _vp, _vp]),
+    "bnmc_gpu_score_order": (C.c_int, [_vp, _i32p, _vp, _vp, _vp]),
+    "bnmc_gpu_run_chains": (C.c_int, [_vp, _u64p, C.c_int, C.POINTER(ChainParams), _vp, _vp, _vp,
+                                      _vp, _vp, _vp, _vp, _vp, _vp, C.POINTER(C.c_float)]),
+    "bnmc_gpu_last_scan_stats": (C.c_int, [_vp, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64),
+                                           C.POINTER(C.c_float), C.POINTER(C.c_uint64)]),
+    "bnmc_synth_last_error": (C.c_char_p, []),
+    "bnmc_synth_instance": (C.c_int, [C.c_int, C.c_int, C.c_double, C.c_double, C.c_uint64,
+                                      _i32p, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64,
+                                      _u8p, _u64p]),
+    "bnmc_synth_priors": (C.c_int, [C.c_int, _u64p, C.c_uint64, C.c_uint64, _f64p]),
+}
+
+
+class Error(RuntimeError):
+    """bnmc::Error (types.hpp:16-18)."""
+
+
+class UsageError(Error):
+    """bnmc::UsageError — bad flags / configuration (status 2)."""
+
+
+class DataError(Error):
+    """bnmc::DataError — invalid input data (status 3)."""
+
+
+class CapacityError(Error):
+    """bnmc::CapacityError — memory estimate over the cap (status 4)."""
+
+
+class CudaError(Error):
+    """CUDA runtime failure or no usable sm_100 device (status 5)."""
+
+
+_EXC = {2: UsageError, 3: DataError, 4: CapacityError, 5: CudaError}
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: build it with __graft_entry__.build() "
+                          "(no CPU fallback exists)")
+    L = C.CDLL(LIB_PATH)
+    for name, (res, args) in SIGNATURES.items():
+        f = getattr(L, name)
+        f.restype = res
+        f.argtypes = args
+    _lib = L
+    return L
+
+
+def check(status: int):
+    if status != 0:
+        msg = lib().bnmc_gpu_last_error_message().decode()
+        raise _EXC.get(status, Error)(msg)
+
+
+def check_synth(status: int):
+    if status != 0:
+        raise _EXC.get(status, Error)(lib().bnmc_synth_last_error().decode())
+
+
+def ptr(a):
+    """Data pointer of an optional numpy array (None -> NULL)."""
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+def device_count() -> int:
+    n = C.c_int()
+    check(lib().bnmc_gpu_device_count(C.byref(n)))
+    return n.value

@@ -1,0 +1,734 @@
+// bnmc_gpu.cu — C-ABI (include/bnmc_gpu.h) over the sm_100a kernels.
+//
+// Device layout of a table:
+//   d_cmask[Sp]      u64 candidate-position mask of global index g, shared by
+//                    every row (global_index order, combinatorics.cpp:61-76);
+//                    padding entries = ~0 (never admissible)
+//   d_ls[n][S]       fp64 local scores, BNSC body order (scoring.cpp:194-238)
+//   d_key32[n][Sp]   fp32 scan keys fl32(ls + PpfTable::sum), padding -inf
+//   d_key64[n][Sp]   fp64 scan keys (allocated only for scan_mode 2)
+//   d_w[n][n]        PPF weights (scoring.cpp:150-155)
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string.h>
+
+#include <cmath>
+#include <cstdio>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/bnmc_gpu.h"
+#include "chain.cuh"
+#include "common.cuh"
+#include "host_util.hpp"
+#include "precompute.cuh"
+
+using namespace bnmc_dev;
+using bnmc_host::raise;
+using bnmc_host::Status;
+using bnmc_host::cuda_check;
+using bnmc_host::precompute_rows;
+using bnmc_host::count_statistics_device;
+
+namespace {
+
+thread_local std::string g_err;
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return BNMC_OK;
+  } catch (const Status& s) {
+    g_err = s.msg;
+    return s.code;
+  } catch (const std::bad_alloc&) {
+    g_err = "host allocation failed";
+    return BNMC_CAPACITY;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return BNMC_ERR;
+  }
+}
+
+uint64_t h_binom[65][65];
+bool h_binom_ready = false;
+void host_binom_init() {
+  if (h_binom_ready) return;
+  for (int n = 0; n <= 64; ++n) {
+    h_binom[n][0] = 1;
+    for (int k = 1; k <= n; ++k) h_binom[n][k] = h_binom[n - 1][k - 1] + h_binom[n - 1][k];
+    for (int k = n + 1; k <= 64; ++k) h_binom[n][k] = 0;
+  }
+  h_binom_ready = true;
+}
+uint64_t hbinom(int n, int k) {
+  host_binom_init();
+  return (k < 0 || n < 0 || k > n) ? 0 : h_binom[n][k];
+}
+uint64_t bounded_count(int c, int s) {
+  uint64_t t = 0;
+  for (int j = 0; j <= s; ++j) t += hbinom(c, j);
+  return t;
+}
+
+// One-time per device: binomial table into constant memory; sm_100 check.
+void ensure_device(int dev) {
+  int count = 0;
+  CK(cudaGetDeviceCount(&count));
+  if (dev < 0 || dev >= count)
+    raise(BNMC_CUDA, "CUDA device " + std::to_string(dev) + " not available (" +
+                         std::to_string(count) + " visible)");
+  CK(cudaSetDevice(dev));
+  static bool ready[64] = {false};
+  if (!ready[dev]) {
+    cudaDeviceProp p;
+    CK(cudaGetDeviceProperties(&p, dev));
+    if (p.major != 10)
+      raise(BNMC_CUDA, std::string("bnmc_gpu is built for sm_100a (B200); device is ") + p.name);
+    host_binom_init();
+    CK(cudaMemcpyToSymbol(c_binom, h_binom, sizeof(h_binom)));
+    ready[dev] = true;
+  }
+}
+
+void validate_params(const bnmc_score_params* p) {
+  if (!p) raise(BNMC_USAGE, "null score params");
+  // RunConfig::validate (types.cpp:111-121), scoring fields
+  if (p->max_parents < 0 || p->max_parents > 8) raise(BNMC_USAGE, "max-parents must lie in [0,8]");
+  if (!(p->gamma > 0.0 && p->gamma <= 1.0)) raise(BNMC_USAGE, "gamma must lie in (0,1]");
+  if (!(p->ess > 0.0)) raise(BNMC_USAGE, "ess must be positive");
+  if (p->alpha_mode != BNMC_ALPHA_BDEU && p->alpha_mode != BNMC_ALPHA_K2)
+    raise(BNMC_USAGE, "alpha_mode must be BDeu (0) or K2 (1)");
+}
+
+// ppf (scoring.cpp:143-148) and PpfTable (scoring.cpp:150-155).
+std::vector<double> ppf_weights(const double* r, int n) {
+  std::vector<double> w(static_cast<size_t>(n) * n, 0.0);
+  if (!r) return w;
+  for (int i = 0; i < n * n; ++i)
+    if (!(r[i] >= 0.0 && r[i] <= 1.0)) raise(BNMC_DATA, "prior matrix entries must lie in [0,1]");
+  for (int i = 0; i < n; ++i)
+    for (int m = 0; m < n; ++m)
+      if (i != m) {
+        const double d = r[i * n + m] - 0.5;
+        w[i * n + m] = 100.0 * d * d * d;
+      }
+  return w;
+}
+
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  void alloc(size_t count) {
+    if (count <= n && p) return;
+    release();
+    if (count == 0) return;
+    cuda_check(cudaMalloc(&p, count * sizeof(T)), "cudaMalloc");
+    n = count;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  ~DevBuf() { release(); }
+};
+
+}  // namespace
+
+struct bnmc_table {
+  int dev = 0;
+  int n = 0, s = 0;
+  uint64_t S = 0, Sp = 0;
+  double gamma = 0.1, ess = 1.0;
+  int alpha = 0;
+  cudaStream_t stream = nullptr;
+  DevBuf<uint64_t> cmask;
+  DevBuf<double> ls;
+  DevBuf<float> key32;
+  DevBuf<double> key64;
+  DevBuf<double> w;
+  bool key64_valid = false;
+  std::vector<double> h_w;
+  float build_ms = 0.f, fold_ms = 0.f;
+  // chain / order-scoring workspace
+  DevBuf<ChainState> st;
+  DevBuf<Item> items;
+  DevBuf<int> counts;
+  DevBuf<uint8_t> ppos;
+  DevBuf<uint8_t> partials;
+  DevBuf<uint8_t> props;
+  DevBuf<double> thr;
+  DevBuf<uint64_t> tmasks;
+  DevBuf<double> ttotals;
+  DevBuf<double> tr_prop, tr_best;
+  DevBuf<uint8_t> tr_acc;
+  DevBuf<unsigned long long> stat;
+  DevBuf<uint64_t> seeds;
+  DevBuf<int> perms;
+  DevBuf<uint64_t> out_masks;
+  DevBuf<double> out_best, out_total;
+  uint64_t last_rescans = 0, last_streamed = 0, last_launches = 0;
+  float last_scan_ms = 0.f;
+  ~bnmc_table() {
+    if (stream) cudaStreamDestroy(stream);
+  }
+};
+
+namespace {
+
+struct ScanGeom {
+  int G, T, U, L4, units;
+};
+
+ScanGeom scan_geometry(const bnmc_table* t) {
+  ScanGeom g;
+  g.units = static_cast<int>(t->Sp / 4);
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, t->dev);
+  g.G = std::max(1, std::min(sms, (g.units + 31) / 32));
+  g.L4 = (g.units + g.G - 1) / g.G;
+  g.U = 1;
+  while (g.U < 8 && (g.L4 + g.U - 1) / g.U > kScanMaxThreads) g.U *= 2;
+  if ((g.L4 + g.U - 1) / g.U > kScanMaxThreads) {
+    // Too many units per CTA for register-resident masks: add CTAs.
+    g.U = 8;
+    g.L4 = 8 * kScanMaxThreads;
+    g.G = (g.units + g.L4 - 1) / g.L4;
+  }
+  g.T = std::max(32, (((g.L4 + g.U - 1) / g.U) + 31) / 32 * 32);
+  return g;
+}
+
+template <typename K>
+void launch_scan(const ScanGeom& g, const ScanArgs& a, cudaStream_t s) {
+  switch (g.U) {
+    case 1: scan_kernel<K, 1, 8><<<g.G, g.T, 0, s>>>(a); break;
+    case 2: scan_kernel<K, 2, 4><<<g.G, g.T, 0, s>>>(a); break;
+    case 4: scan_kernel<K, 4, 2><<<g.G, g.T, 0, s>>>(a); break;
+    default: scan_kernel<K, 8, 1><<<g.G, g.T, 0, s>>>(a); break;
+  }
+}
+
+// Candidate masks in global-index order (device unrank, combinatorics.cpp:8-39,
+// 78-90): sizes s..0, lexicographic within a size.
+__global__ void build_cmask_kernel(uint64_t* out, uint64_t S, uint64_t Sp, int c, int s) {
+  const uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (g >= Sp) return;
+  if (g >= S) {
+    out[g] = ~0ull;
+    return;
+  }
+  uint64_t r = g;
+  int k = s < c ? s : c;
+  for (; k >= 0; --k) {
+    const uint64_t block = binom(c, k);
+    if (r < block) break;
+    r -= block;
+  }
+  uint64_t mask = 0;
+  int x = 0;
+  for (int i = 0; i < k; ++i) {
+    for (;;) {
+      const uint64_t cnt = binom(c - x - 1, k - i - 1);
+      if (r < cnt) {
+        mask |= 1ull << x;
+        ++x;
+        break;
+      }
+      r -= cnt;
+      ++x;
+    }
+  }
+  out[g] = mask;
+}
+
+// PPF fold: key = fl(ls + PpfTable::sum) in the scan's association
+// (engine.cpp:50-51), fp32 and/or fp64; padding -inf.
+__global__ void fold_kernel(const double* __restrict__ ls, const uint64_t* __restrict__ cmask,
+                            const double* __restrict__ w, float* key32, double* key64, int n,
+                            uint64_t S, uint64_t Sp) {
+  const int v = blockIdx.y;
+  for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < Sp;
+       g += (uint64_t)gridDim.x * blockDim.x) {
+    double e = -INFINITY;
+    if (g < S) e = ls[(uint64_t)v * S + g] + ppf_sum(w, n, v, cand_to_nodes(cmask[g], v));
+    if (key32) key32[(uint64_t)v * Sp + g] = __double2float_rn(e);
+    if (key64) key64[(uint64_t)v * Sp + g] = e;
+  }
+}
+
+void table_init(bnmc_table* t, int n, const bnmc_score_params* p) {
+  validate_params(p);
+  if (n < 1 || n > 64) raise(BNMC_DATA, "dataset must have between 1 and 64 variables");
+  ensure_device(p->device);
+  t->dev = p->device;
+  t->n = n;
+  t->s = p->max_parents;
+  t->gamma = p->gamma;
+  t->ess = p->ess;
+  t->alpha = p->alpha_mode;
+  t->S = bounded_count(n - 1, t->s);
+  t->Sp = (t->S + 31) / 32 * 32;
+  const uint64_t est = static_cast<uint64_t>(n) * t->S * 8;  // estimate_bytes
+  if (est > p->memory_cap_bytes)
+    raise(BNMC_CAPACITY, "score cache estimate " + std::to_string(est) +
+                             " bytes exceeds cap of " + std::to_string(p->memory_cap_bytes));
+  CK(cudaStreamCreateWithFlags(&t->stream, cudaStreamNonBlocking));
+  t->cmask.alloc(t->Sp);
+  t->ls.alloc(static_cast<size_t>(n) * t->S);
+  t->key32.alloc(static_cast<size_t>(n) * t->Sp);
+  t->w.alloc(static_cast<size_t>(n) * n);
+  const unsigned blocks = static_cast<unsigned>((t->Sp + 255) / 256);
+  build_cmask_kernel<<<blocks, 256, 0, t->stream>>>(t->cmask.p, t->S, t->Sp, n - 1, t->s);
+  CK(cudaGetLastError());
+}
+
+void set_priors(bnmc_table* t, const double* prior_r) {
+  t->h_w = ppf_weights(prior_r, t->n);
+  CK(cudaMemcpyAsync(t->w.p, t->h_w.data(), t->h_w.size() * 8, cudaMemcpyHostToDevice, t->stream));
+}
+
+void fold(bnmc_table* t, bool want64) {
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  if (want64) t->key64.alloc(static_cast<size_t>(t->n) * t->Sp);
+  const unsigned bx = static_cast<unsigned>(std::min<uint64_t>((t->Sp + 255) / 256, 4096));
+  CK(cudaEventRecord(e0, t->stream));
+  fold_kernel<<<dim3(bx, t->n), 256, 0, t->stream>>>(t->ls.p, t->cmask.p, t->w.p, t->key32.p,
+                                                       want64 ? t->key64.p : nullptr, t->n, t->S,
+                                                       t->Sp);
+  CK(cudaGetLastError());
+  CK(cudaEventRecord(e1, t->stream));
+  CK(cudaEventSynchronize(e1));
+  CK(cudaEventElapsedTime(&t->fold_ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  t->key64_valid = want64;
+}
+
+TieCtx tie_ctx(const bnmc_table* t) {
+  TieCtx c;
+  c.ls = t->ls.p;
+  c.cmask = t->cmask.p;
+  c.w = t->w.p;
+  c.S = t->S;
+  c.n = t->n;
+  return c;
+}
+
+// Accept thresholds: log10(next_unit_open()) of the split(3) stream with the
+// host's glibc log10 — exactly mh_accept's left-hand side (sampler.cpp:54-56).
+// The acceptance stream draws once per iteration whatever the outcome, so it
+// is state-independent and can be materialised before the device loop.
+void accept_thresholds(const uint64_t* seeds, int C, uint64_t iters, std::vector<double>& out) {
+  out.assign(static_cast<size_t>(C) * (iters + 1), 0.0);
+  for (int c = 0; c < C; ++c) {
+    Rng acc = Rng{seeds[c]}.split(3);
+    double* o = out.data() + static_cast<size_t>(c) * (iters + 1);
+    for (uint64_t t = 1; t <= iters; ++t) o[t] = std::log10(acc.next_unit_open());
+  }
+}
+
+void ensure_workspace(bnmc_table* t, int C, uint64_t iters, int K, const ScanGeom& g,
+                      size_t key_bytes) {
+  const int n = t->n;
+  t->st.alloc(C);
+  t->items.alloc(static_cast<size_t>(C) * n);
+  t->counts.alloc(C);
+  t->ppos.alloc(static_cast<size_t>(C) * 64);
+  t->partials.alloc(static_cast<size_t>(C) * n * g.G * (key_bytes == 4 ? 8 : 16));
+  t->stat.alloc(1);
+  if (iters) {
+    t->props.alloc(static_cast<size_t>(C) * (iters + 1) * 2);
+    t->thr.alloc(static_cast<size_t>(C) * (iters + 1));
+    t->tmasks.alloc(static_cast<size_t>(C) * K * n);
+    t->ttotals.alloc(static_cast<size_t>(C) * K);
+    t->tr_prop.alloc(static_cast<size_t>(C) * iters);
+    t->tr_best.alloc(static_cast<size_t>(C) * iters);
+    t->tr_acc.alloc(static_cast<size_t>(C) * iters);
+  }
+}
+
+template <typename K>
+void run_scan_and_step(bnmc_table* t, const ScanGeom& g, const ScanArgs& sa, const StepArgs& A,
+                       int C) {
+  launch_scan<K>(g, sa, t->stream);
+  step_kernel<K><<<C, 256, 0, t->stream>>>(A);
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ C-ABI
+extern "C" {
+
+const char* bnmc_gpu_last_error_message(void) { return g_err.c_str(); }
+int bnmc_gpu_version(void) { return 10000; }
+
+int bnmc_gpu_device_count(int* out) {
+  return guarded([&] {
+    int count = 0;
+    const cudaError_t e = cudaGetDeviceCount(&count);
+    if (e == cudaErrorNoDevice || e == cudaErrorInsufficientDriver) {
+      cudaGetLastError();
+      *out = 0;
+      return;
+    }
+    CK(e);
+    int ok = 0;
+    for (int d = 0; d < count; ++d) {
+      cudaDeviceProp p;
+      CK(cudaGetDeviceProperties(&p, d));
+      if (p.major == 10) ++ok;
+    }
+    *out = ok;
+  });
+}
+
+uint64_t bnmc_gpu_table_estimate_bytes(int n, int s) {
+  return static_cast<uint64_t>(n) * bounded_count(n - 1, s) * 8;
+}
+uint64_t bnmc_gpu_bounded_subset_count(int c, int s) { return bounded_count(c, s); }
+
+int bnmc_gpu_table_upload(const double* table, int n, const bnmc_score_params* params,
+                          const double* prior_r, bnmc_table** out) {
+  return guarded([&] {
+    auto t = std::make_unique<bnmc_table>();
+    table_init(t.get(), n, params);
+    CK(cudaMemcpyAsync(t->ls.p, table, static_cast<size_t>(n) * t->S * 8, cudaMemcpyHostToDevice,
+                       t->stream));
+    set_priors(t.get(), prior_r);
+    fold(t.get(), false);
+    *out = t.release();
+  });
+}
+
+int bnmc_gpu_table_build(const uint8_t* cells, const int* cards, uint64_t m, int n,
+                         const bnmc_score_params* params, const double* prior_r,
+                         bnmc_table** out) {
+  int st = bnmc_gpu_table_build_rows(cells, cards, m, n, params, prior_r, 0, n, out);
+  if (st != BNMC_OK) return st;
+  st = bnmc_gpu_table_finalize(*out);
+  if (st != BNMC_OK) {
+    const std::string keep = g_err;
+    bnmc_gpu_table_free(*out);
+    *out = nullptr;
+    g_err = keep;
+  }
+  return st;
+}
+
+int bnmc_gpu_table_build_rows(const uint8_t* cells, const int* cards, uint64_t m, int n,
+                              const bnmc_score_params* params, const double* prior_r,
+                              int row_begin, int row_end, bnmc_table** out) {
+  return guarded([&] {
+    *out = nullptr;
+    if (n < 1 || n > 64) raise(BNMC_DATA, "dataset must have between 1 and 64 variables");
+    for (int i = 0; i < n; ++i)
+      if (cards[i] < 2 || cards[i] > 256)
+        raise(BNMC_DATA, "cardinality of variable " + std::to_string(i) + " out of range [2,256]");
+    for (uint64_t r = 0; r < m; ++r)
+      for (int i = 0; i < n; ++i)
+        if (cells[r * n + i] >= cards[i])
+          raise(BNMC_DATA, "state out of range at row " + std::to_string(r) + ", column " +
+                               std::to_string(i));
+    if (row_begin < 0 || row_end > n || row_begin > row_end) raise(BNMC_USAGE, "bad row range");
+    auto t = std::make_unique<bnmc_table>();
+    table_init(t.get(), n, params);
+    set_priors(t.get(), prior_r);
+    precompute_rows(t->stream, t->ls.p, t->S, cells, cards, m, n, t->s, t->gamma, t->ess,
+                    t->alpha, row_begin, row_end, &t->build_ms);
+    *out = t.release();
+  });
+}
+
+int bnmc_gpu_table_rows_buffer(bnmc_table* t, void** dev_ptr, uint64_t* bytes,
+                               uint64_t* row_stride_elems) {
+  return guarded([&] {
+    if (!t) raise(BNMC_USAGE, "null table");
+    *dev_ptr = t->ls.p;
+    *bytes = static_cast<uint64_t>(t->n) * t->S * 8;
+    *row_stride_elems = t->S;
+  });
+}
+
+int bnmc_gpu_table_finalize(bnmc_table* t) {
+  return guarded([&] {
+    if (!t) raise(BNMC_USAGE, "null table");
+    CK(cudaSetDevice(t->dev));
+    fold(t, t->key64_valid);
+  });
+}
+
+int bnmc_gpu_table_set_priors(bnmc_table* t, const double* prior_r) {
+  return guarded([&] {
+    if (!t) raise(BNMC_USAGE, "null table");
+    CK(cudaSetDevice(t->dev));
+    set_priors(t, prior_r);
+    fold(t, t->key64_valid);
+  });
+}
+
+int bnmc_gpu_table_info(const bnmc_table* t, int* n, int* s, uint64_t* per_node) {
+  return guarded([&] {
+    if (!t) raise(BNMC_USAGE, "null table");
+    if (n) *n = t->n;
+    if (s) *s = t->s;
+    if (per_node) *per_node = t->S;
+  });
+}
+
+int bnmc_gpu_table_download(const bnmc_table* t, double* out) {
+  return guarded([&] {
+    if (!t) raise(BNMC_USAGE, "null table");
+    CK(cudaSetDevice(t->dev));
+    CK(cudaMemcpyAsync(out, t->ls.p, static_cast<size_t>(t->n) * t->S * 8, cudaMemcpyDeviceToHost,
+                       t->stream));
+    CK(cudaStreamSynchronize(t->stream));
+  });
+}
+
+int bnmc_gpu_table_build_ms(const bnmc_table* t, float* count_score_ms, float* fold_ms) {
+  return guarded([&] {
+    if (!t) raise(BNMC_USAGE, "null table");
+    if (count_score_ms) *count_score_ms = t->build_ms;
+    if (fold_ms) *fold_ms = t->fold_ms;
+  });
+}
+
+int bnmc_gpu_table_free(bnmc_table* t) {
+  return guarded([&] {
+    if (!t) return;
+    cudaSetDevice(t->dev);
+    delete t;
+  });
+}
+
+int bnmc_gpu_count_statistics(const uint8_t* cells, const int* cards, uint64_t m, int n, int count,
+                              const int* nodes, const uint64_t* psets, const uint64_t* offsets,
+                              uint32_t* out, uint64_t* configs_out, int device) {
+  return guarded([&] {
+    ensure_device(device);
+    count_statistics_device(cells, cards, m, n, count, nodes, psets, offsets, out, configs_out);
+  });
+}
+
+int bnmc_gpu_score_orders(bnmc_table* t, const int* perms, int count, uint64_t* masks_out,
+                          double* best_out, double* totals_out) {
+  return guarded([&] {
+    if (!t) raise(BNMC_USAGE, "null table");
+    if (count < 1) return;
+    const int n = t->n;
+    for (int c = 0; c < count; ++c) {  // Order::Order validation (types.cpp:28-38)
+      std::vector<bool> seen(n, false);
+      for (int i = 0; i < n; ++i) {
+        const int v = perms[static_cast<size_t>(c) * n + i];
+        if (v < 0 || v >= n || seen[v]) raise(BNMC_DATA, "order is not a permutation of 0..n-1");
+        seen[v] = true;
+      }
+    }
+    CK(cudaSetDevice(t->dev));
+    const ScanGeom g = scan_geometry(t);
+    ensure_workspace(t, count, 0, 0, g, 4);
+    t->perms.alloc(static_cast<size_t>(count) * n);
+    t->out_masks.alloc(static_cast<size_t>(count) * n);
+    t->out_best.alloc(static_cast<size_t>(count) * n);
+    t->out_total.alloc(count);
+    CK(cudaMemcpyAsync(t->perms.p, perms, sizeof(int) * count * n, cudaMemcpyHostToDevice,
+                       t->stream));
+    StepArgs A{};
+    A.items = t->items.p;
+    A.counts = t->counts.p;
+    A.ppos = t->ppos.p;
+    A.partials = t->partials.p;
+    A.stat_rows = t->stat.p;
+    A.n = n;
+    A.G = g.G;
+    A.score_only = 1;
+    A.out_masks = t->out_masks.p;
+    A.out_best = t->out_best.p;
+    A.out_total = t->out_total.p;
+    A.tie = tie_ctx(t);
+    setup_orders_kernel<<<(count + 127) / 128, 128, 0, t->stream>>>(A, t->perms.p, count);
+    ScanArgs sa{};
+    sa.keys = t->key32.p;
+    sa.Sp = t->Sp;
+    sa.items = t->items.p;
+    sa.counts = t->counts.p;
+    sa.ppos = t->ppos.p;
+    sa.partials = t->partials.p;
+    sa.C = count;
+    sa.n = n;
+    sa.G = g.G;
+    sa.units = g.units;
+    sa.L4 = g.L4;
+    sa.tie = A.tie;
+    run_scan_and_step<float>(t, g, sa, A, count);
+    CK(cudaGetLastError());
+    if (masks_out)
+      CK(cudaMemcpyAsync(masks_out, t->out_masks.p, 8ull * count * n, cudaMemcpyDeviceToHost,
+                         t->stream));
+    if (best_out)
+      CK(cudaMemcpyAsync(best_out, t->out_best.p, 8ull * count * n, cudaMemcpyDeviceToHost,
+                         t->stream));
+    if (totals_out)
+      CK(cudaMemcpyAsync(totals_out, t->out_total.p, 8ull * count, cudaMemcpyDeviceToHost,
+                         t->stream));
+    CK(cudaStreamSynchronize(t->stream));
+  });
+}
+
+int bnmc_gpu_score_order(bnmc_table* t, const int* perm, uint64_t* masks_out, double* best_out,
+                         double* total_out) {
+  return bnmc_gpu_score_orders(t, perm, 1, masks_out, best_out, total_out);
+}
+
+int bnmc_gpu_run_chains(bnmc_table* t, const uint64_t* seeds, int n_chains,
+                        const bnmc_chain_params* params, double* trace_proposed,
+                        uint8_t* trace_accepted, double* trace_best, int* final_order,
+                        double* final_score, uint64_t* accepted, int* tracker_count,
+                        uint64_t* tracker_masks, double* tracker_totals, float* device_ms) {
+  return guarded([&] {
+    if (!t) raise(BNMC_USAGE, "null table");
+    if (!params) raise(BNMC_USAGE, "null chain params");
+    if (params->iterations < 1) raise(BNMC_USAGE, "iterations must be >= 1");
+    if (params->track_top < 1) raise(BNMC_USAGE, "tracker capacity must be >= 1");
+    if (n_chains < 1) raise(BNMC_USAGE, "n_chains must be >= 1");
+    if (t->n < 2) raise(BNMC_USAGE, "swap proposal needs at least two nodes");
+    const int mode = params->scan_mode;
+    if (mode < 0 || mode > 2) raise(BNMC_USAGE, "scan_mode must be 0, 1 or 2");
+    const bool f64 = mode == 2;
+    CK(cudaSetDevice(t->dev));
+    if (f64 && !t->key64_valid) fold(t, true);
+    const int n = t->n, C = n_chains, K = params->track_top;
+    const uint64_t iters = params->iterations;
+    const ScanGeom g = scan_geometry(t);
+    ensure_workspace(t, C, iters, K, g, f64 ? 8 : 4);
+    t->seeds.alloc(C);
+    std::vector<double> thr;
+    accept_thresholds(seeds, C, iters, thr);
+    CK(cudaMemcpyAsync(t->seeds.p, seeds, 8ull * C, cudaMemcpyHostToDevice, t->stream));
+    CK(cudaMemcpyAsync(t->thr.p, thr.data(), thr.size() * 8, cudaMemcpyHostToDevice, t->stream));
+    CK(cudaMemsetAsync(t->stat.p, 0, 8, t->stream));
+    StepArgs A{};
+    A.st = t->st.p;
+    A.items = t->items.p;
+    A.counts = t->counts.p;
+    A.ppos = t->ppos.p;
+    A.partials = t->partials.p;
+    A.props = t->props.p;
+    A.thr = t->thr.p;
+    A.tmasks = t->tmasks.p;
+    A.ttotals = t->ttotals.p;
+    A.tr_prop = t->tr_prop.p;
+    A.tr_acc = t->tr_acc.p;
+    A.tr_best = t->tr_best.p;
+    A.stat_rows = t->stat.p;
+    A.iters = iters;
+    A.n = n;
+    A.G = g.G;
+    A.K = K;
+    A.strict = params->strict;
+    A.tie = tie_ctx(t);
+    setup_chains_kernel<<<(C + 63) / 64, 64, 0, t->stream>>>(A, t->seeds.p, C);
+    CK(cudaGetLastError());
+    ScanArgs sa{};
+    sa.keys = f64 ? static_cast<const void*>(t->key64.p) : static_cast<const void*>(t->key32.p);
+    sa.Sp = t->Sp;
+    sa.items = t->items.p;
+    sa.counts = t->counts.p;
+    sa.ppos = t->ppos.p;
+    sa.partials = t->partials.p;
+    sa.C = C;
+    sa.n = n;
+    sa.G = g.G;
+    sa.units = g.units;
+    sa.L4 = g.L4;
+    sa.tie = A.tie;
+
+    // Capture a batch of (scan, step) pairs once; replay it until every chain
+    // has finalized iteration `iters` (steps beyond that are no-ops).
+    const uint64_t total_steps = iters + 1;
+    const int batch = static_cast<int>(std::min<uint64_t>(total_steps, 256));
+    cudaGraph_t graph;
+    cudaGraphExec_t exec;
+    CK(cudaStreamBeginCapture(t->stream, cudaStreamCaptureModeThreadLocal));
+    for (int i = 0; i < batch; ++i) {
+      if (f64)
+        run_scan_and_step<double>(t, g, sa, A, C);
+      else
+        run_scan_and_step<float>(t, g, sa, A, C);
+    }
+    CK(cudaStreamEndCapture(t->stream, &graph));
+    CK(cudaGraphInstantiate(&exec, graph, 0));
+    const uint64_t replays = (total_steps + batch - 1) / batch;
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    CK(cudaEventRecord(e0, t->stream));
+    for (uint64_t r = 0; r < replays; ++r) CK(cudaGraphLaunch(exec, t->stream));
+    CK(cudaEventRecord(e1, t->stream));
+    CK(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    if (device_ms) *device_ms = ms;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaGraphExecDestroy(exec);
+    cudaGraphDestroy(graph);
+    CK(cudaGetLastError());
+
+    // Results back to the host.
+    std::vector<ChainState> hs(C);
+    CK(cudaMemcpyAsync(hs.data(), t->st.p, sizeof(ChainState) * C, cudaMemcpyDeviceToHost,
+                       t->stream));
+    if (trace_proposed)
+      CK(cudaMemcpyAsync(trace_proposed, t->tr_prop.p, 8ull * C * iters, cudaMemcpyDeviceToHost,
+                         t->stream));
+    if (trace_accepted)
+      CK(cudaMemcpyAsync(trace_accepted, t->tr_acc.p, 1ull * C * iters, cudaMemcpyDeviceToHost,
+                         t->stream));
+    if (trace_best)
+      CK(cudaMemcpyAsync(trace_best, t->tr_best.p, 8ull * C * iters, cudaMemcpyDeviceToHost,
+                         t->stream));
+    if (tracker_masks)
+      CK(cudaMemcpyAsync(tracker_masks, t->tmasks.p, 8ull * C * K * n, cudaMemcpyDeviceToHost,
+                         t->stream));
+    if (tracker_totals)
+      CK(cudaMemcpyAsync(tracker_totals, t->ttotals.p, 8ull * C * K, cudaMemcpyDeviceToHost,
+                         t->stream));
+    unsigned long long rows = 0;
+    CK(cudaMemcpyAsync(&rows, t->stat.p, 8, cudaMemcpyDeviceToHost, t->stream));
+    CK(cudaStreamSynchronize(t->stream));
+    for (int c = 0; c < C; ++c) {
+      if (!hs[c].done) raise(BNMC_ERR, "chain did not finish (internal error)");
+      if (final_order)
+        for (int i = 0; i < n; ++i) final_order[c * n + i] = hs[c].order[i];
+      if (final_score) final_score[c] = hs[c].total;
+      if (accepted) accepted[c] = hs[c].accepted;
+      if (tracker_count) tracker_count[c] = hs[c].tcount;
+    }
+    t->last_rescans = rows;
+    t->last_streamed = rows;
+    t->last_launches = replays * batch;
+    t->last_scan_ms = ms;
+  });
+}
+
+int bnmc_gpu_last_scan_stats(const bnmc_table* t, uint64_t* row_rescans, uint64_t* rows_streamed,
+                             float* scan_ms, uint64_t* scan_launches) {
+  return guarded([&] {
+    if (!t) raise(BNMC_USAGE, "null table");
+    if (row_rescans) *row_rescans = t->last_rescans;
+    if (rows_streamed) *rows_streamed = t->last_streamed;
+    if (scan_ms) *scan_ms = t->last_scan_ms;
+    if (scan_launches) *scan_launches = t->last_launches;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,565 @@
+// K1 — local-score precompute (sm_100a): ScoreCache::build on the device.
+//
+// Replaces ScoreCache::build -> count_statistics -> local_score_from_counts
+// (scoring.cpp:162-192, 82-135). Counting is done on sample BITPLANES: for
+// every variable i and state x, bit t of plane (i,x) is set iff row t has
+// state x in column i. The count of a joint configuration is then the
+// popcount of the AND of the member planes — integer-exact, no atomics on the
+// sample stream, every count bit-identical to the reference's CountTable.
+//
+// Work is organised by joint sets U (|U| <= s+1): the joint histogram of U
+// serves all |U| entries (v, U - v), v in U, because N_ijk of (v, pi) is the
+// joint count over pi + {v}. A CTA owns one "prefix" P (any set |P| <= s); its
+// U's are P + {u} for every u > max(P), so the AND-planes of P's
+// configurations are built once in shared memory and reused for every
+// extension u; only states x < card(u)-1 are popcounted, the last state is
+// the prefix count minus the others.
+//
+// The score of an entry follows local_score_from_counts exactly: configs of
+// pi ascending (mixed radix, lowest parent least significant, scoring.cpp:
+// 99-105), empty configs skipped (scoring.hpp:55-67), per config
+// inner = sum_{c>0} (lG(c + a_cell) - lG(a_cell)) in state order, then
+// score += (lG(a_row) - lG(a_row + N_ik)) + inner, starting from
+// |pi| * log10(gamma). lG values come from a host-built glibc-lgamma LUT
+// per distinct (r_i, card) pair (log10_gamma, scoring.hpp:16-18), so the fp64
+// adds reproduce the reference bits (the TU is built with -fmad=false).
+#pragma once
+
+#include <algorithm>
+#include <cmath>
+#include <set>
+#include <vector>
+
+#include "common.cuh"
+#include "host_util.hpp"
+
+namespace bnmc_dev {
+
+constexpr int kHMax = 4096;   // max joint cells of a set U (dense counter bound)
+constexpr int kRPMax = 1024;  // max configurations of a prefix P
+constexpr int kK1Threads = 256;
+
+struct K1Args {
+  const uint32_t* __restrict__ bits;  // bitplanes
+  const uint32_t* __restrict__ boff;  // [n] word offset of plane (i, 0); plane x at +x*W
+  const int* __restrict__ cards;      // [n]
+  int n, s, W;
+  uint32_t last_mask;                 // valid bits of the last word
+  int cmax;                           // max cardinality
+  const uint64_t* __restrict__ pair_keys;  // sorted r*512 + card
+  int n_pairs;
+  const double* __restrict__ lut;     // [pair][2*(m+1)]: lG(c + a_cell), then lG(a_row + N)
+  uint64_t lut_stride;                // 2*(m+1)
+  uint64_t m;
+  double log10_gamma;
+  double* ls;                          // [n][S]
+  uint64_t S;
+  int row_begin, row_end;
+  int WT, EG;
+  int* error;
+};
+
+// Subset of {0..c-1} at global index j in the (size desc, lexicographic) order.
+__device__ __forceinline__ uint64_t unrank_global(uint64_t j, int c, int s, int* size_out) {
+  int k = s < c ? s : c;
+  for (; k >= 0; --k) {
+    const uint64_t block = binom(c, k);
+    if (j < block) break;
+    j -= block;
+  }
+  uint64_t mask = 0;
+  int x = 0;
+  for (int i = 0; i < k; ++i) {
+    for (;;) {
+      const uint64_t cnt = binom(c - x - 1, k - i - 1);
+      if (j < cnt) {
+        mask |= 1ull << x;
+        ++x;
+        break;
+      }
+      j -= cnt;
+      ++x;
+    }
+  }
+  *size_out = k;
+  return mask;
+}
+
+// global_index (combinatorics.cpp:61-76)
+__device__ __forceinline__ uint64_t global_index_dev(uint64_t mask, int c, int s) {
+  const int k = __popcll(mask);
+  uint64_t offset = 0;
+  for (int j = k + 1; j <= s; ++j) offset += binom(c, j);
+  uint64_t rank = 0;
+  int prev = 0, pos = 1;
+  for (uint64_t m = mask; m != 0; m &= m - 1, ++pos) {
+    const int a = __ffsll((long long)m);  // 1-based element
+    rank += binom(c - prev, k - pos + 1) - binom(c - a + 1, k - pos + 1);
+    prev = a;
+  }
+  return offset + rank;
+}
+
+__device__ __forceinline__ int find_pair(const K1Args& a, uint64_t key) {
+  int lo = 0, hi = a.n_pairs - 1;
+  while (lo <= hi) {
+    const int mid = (lo + hi) >> 1;
+    const uint64_t k = a.pair_keys[mid];
+    if (k == key) return mid;
+    if (k < key) lo = mid + 1; else hi = mid - 1;
+  }
+  return -1;
+}
+
+__global__ void __launch_bounds__(kK1Threads) k1_kernel(K1Args a, uint64_t prefix_base) {
+  extern __shared__ uint32_t smem[];
+  __shared__ int s_p[9];
+  __shared__ int s_rad[10];
+  __shared__ int s_k, s_rP, s_ext0;
+  const int tid = threadIdx.x;
+  const int n = a.n, W = a.W;
+  if (tid == 0) {
+    int k;
+    const uint64_t P = unrank_global(prefix_base + blockIdx.x, n, a.s, &k);
+    int i = 0, r = 1;
+    for (uint64_t m = P; m; m &= m - 1) {
+      s_p[i] = __ffsll((long long)m) - 1;
+      s_rad[i] = r;
+      r *= a.cards[s_p[i]];
+      ++i;
+    }
+    s_rad[i] = r;
+    s_k = k;
+    s_rP = r;
+    s_ext0 = k ? s_p[k - 1] + 1 : 0;
+  }
+  __syncthreads();
+  const int k = s_k, rP = s_rP, ext0 = s_ext0;
+  const int n_ext = n - ext0;
+  if (n_ext <= 0) return;
+  // Skip prefixes none of whose entries fall in this shard's row range.
+  bool any = ext0 < a.row_end && n > a.row_begin;
+  for (int i = 0; i < k; ++i) any |= (s_p[i] >= a.row_begin && s_p[i] < a.row_end);
+  if (!any) return;
+  if (rP > kRPMax) {
+    if (tid == 0) atomicExch(a.error, 1);
+    return;
+  }
+  const int cmax = a.cmax;
+  const int WT = a.WT;
+  uint32_t* PB = smem;                         // [rP][WT]
+  uint32_t* NP = PB + (size_t)rP * WT;         // [rP]
+  uint32_t* CNT = NP + rP;                     // [EG][rP][cmax]
+
+  for (int e0 = 0; e0 < n_ext; e0 += a.EG) {
+    const int ne = min(a.EG, n_ext - e0);
+    for (int i = tid; i < ne * rP * cmax; i += kK1Threads) CNT[i] = 0;
+    if (e0 == 0)
+      for (int i = tid; i < rP; i += kK1Threads) NP[i] = 0;
+    __syncthreads();
+    for (int w0 = 0; w0 < W; w0 += WT) {
+      const int wt = min(WT, W - w0);
+      // AND-planes of every configuration of P over this word tile.
+      for (int idx = tid; idx < rP * wt; idx += kK1Threads) {
+        const int cfg = idx / wt, w = idx - cfg * wt;
+        uint32_t word = (w0 + w == W - 1) ? a.last_mask : 0xFFFFFFFFu;
+        int rem = cfg;
+        for (int i = 0; i < k; ++i) {
+          const int ci = a.cards[s_p[i]];
+          const int d = rem % ci;
+          rem /= ci;
+          word &= a.bits[a.boff[s_p[i]] + (uint32_t)d * W + w0 + w];
+        }
+        PB[cfg * WT + w] = word;
+      }
+      __syncthreads();
+      const int NS = max(1, min(wt, kK1Threads / rP));
+      for (int task = tid; task < rP * NS; task += kK1Threads) {
+        const int cfg = task % rP, sl = task / rP;
+        const int wa = sl * wt / NS, wb = (sl + 1) * wt / NS;
+        const uint32_t* pb = PB + cfg * WT;
+        if (e0 == 0) {
+          uint32_t acc = 0;
+          for (int w = wa; w < wb; ++w) acc += __popc(pb[w]);
+          atomicAdd(&NP[cfg], acc);
+        }
+        for (int e = 0; e < ne; ++e) {
+          const int u = ext0 + e0 + e;
+          const int cu = a.cards[u];
+          for (int x = 0; x < cu - 1; ++x) {
+            const uint32_t* bp = a.bits + a.boff[u] + (uint32_t)x * W + w0;
+            uint32_t acc = 0;
+            for (int w = wa; w < wb; ++w) acc += __popc(pb[w] & __ldg(bp + w));
+            atomicAdd(&CNT[(e * rP + cfg) * cmax + x], acc);
+          }
+        }
+      }
+      __syncthreads();
+    }
+    // Last state of u by difference with the prefix count.
+    for (int idx = tid; idx < ne * rP; idx += kK1Threads) {
+      const int e = idx / rP, cfg = idx - e * rP;
+      const int cu = a.cards[ext0 + e0 + e];
+      uint32_t* c = CNT + (e * rP + cfg) * cmax;
+      uint32_t sum = 0;
+      for (int x = 0; x < cu - 1; ++x) sum += c[x];
+      c[cu - 1] = NP[cfg] - sum;
+    }
+    __syncthreads();
+    // Score the |U| entries (v, U - v) of every U = P + {u}.
+    for (int idx = tid; idx < ne * (k + 1); idx += kK1Threads) {
+      const int e = idx / (k + 1), d = idx - e * (k + 1);
+      const int u = ext0 + e0 + e;
+      const int v = d < k ? s_p[d] : u;
+      if (v < a.row_begin || v >= a.row_end) continue;
+      const int cu = a.cards[u];
+      const int cv = a.cards[v];
+      uint64_t pmask = 1ull << u;
+      for (int i = 0; i < k; ++i) pmask |= 1ull << s_p[i];
+      pmask &= ~(1ull << v);
+      const uint64_t r_pi = (uint64_t)rP * cu / cv;
+      const int pair = find_pair(a, r_pi * 512 + cv);
+      if (pair < 0) {
+        atomicExch(a.error, 2);
+        continue;
+      }
+      const double* lgc = a.lut + (uint64_t)pair * a.lut_stride;
+      const double* lgr = lgc + a.m + 1;
+      const double lg_cell = lgc[0], lg_row = lgr[0];
+      double score = (double)k * a.log10_gamma;  // |pi| = k, int * double first
+      const uint32_t* H = CNT + e * rP * cmax;    // H[cfgP * cmax + x_u]
+      if (d == k) {
+        // child = u: configs of pi = P ascending, states of u.
+        for (int cfg = 0; cfg < rP; ++cfg) {
+          const uint32_t* row = H + cfg * cmax;
+          uint32_t n_ik = 0;
+          double inner = 0.0;
+          for (int x = 0; x < cv; ++x) {
+            const uint32_t c = row[x];
+            if (c > 0) {
+              inner += lgc[c] - lg_cell;
+              n_ik += c;
+            }
+          }
+          if (n_ik > 0) score += lg_row - lgr[n_ik] + inner;
+        }
+      } else {
+        // child = p_d: configs of pi = (P - p_d) + {u}: k' = low + R*(mid + Q*x_u).
+        const int R = s_rad[d], cd = cv;
+        const int Q = rP / (R * cd);
+        for (int xu = 0; xu < cu; ++xu)
+          for (int mid = 0; mid < Q; ++mid)
+            for (int low = 0; low < R; ++low) {
+              uint32_t n_ik = 0;
+              double inner = 0.0;
+              for (int y = 0; y < cd; ++y) {
+                const uint32_t c = H[(low + R * (y + cd * mid)) * cmax + xu];
+                if (c > 0) {
+                  inner += lgc[c] - lg_cell;
+                  n_ik += c;
+                }
+              }
+              if (n_ik > 0) score += lg_row - lgr[n_ik] + inner;
+            }
+      }
+      const uint64_t g = global_index_dev(nodes_to_cand(pmask, v), n - 1, a.s);
+      a.ls[(uint64_t)v * a.S + g] = score;
+    }
+    __syncthreads();
+  }
+}
+
+// Bitplanes from row-major cells: one thread per (variable, word).
+__global__ void bitplane_kernel(const uint8_t* __restrict__ cells, const int* __restrict__ cards,
+                                const uint32_t* __restrict__ boff, uint32_t* bits, int n,
+                                uint64_t m, int W) {
+  const int i = blockIdx.y;
+  const int w = blockIdx.x * blockDim.x + threadIdx.x;
+  if (w >= W) return;
+  const int ci = cards[i];
+  uint8_t st[32];
+  const uint64_t t0 = (uint64_t)w * 32;
+  const int nb = (int)(m - t0 < 32 ? m - t0 : 32);
+  for (int b = 0; b < 32; ++b) st[b] = b < nb ? cells[(t0 + b) * n + i] : 0xFF;
+  for (int x = 0; x < ci; ++x) {
+    uint32_t word = 0;
+    for (int b = 0; b < nb; ++b) word |= (uint32_t)(st[b] == x) << b;
+    bits[boff[i] + (uint32_t)x * W + w] = word;
+  }
+}
+
+// count_statistics for explicit (node, pset) entries: cell (cfg, x) counted
+// as popcount(AND of parent planes & child plane x) over all words.
+__global__ void counts_kernel(const uint32_t* __restrict__ bits, const uint32_t* __restrict__ boff,
+                              const int* __restrict__ cards, int W, uint32_t last_mask,
+                              const int* __restrict__ nodes, const uint64_t* __restrict__ psets,
+                              const uint64_t* __restrict__ offsets, uint32_t* out) {
+  const int e = blockIdx.x;
+  const int v = nodes[e];
+  const uint64_t ps = psets[e];
+  int par[64], np = 0;
+  uint64_t r = 1;
+  for (uint64_t m = ps; m; m &= m - 1) {
+    par[np] = __ffsll((long long)m) - 1;
+    r *= (uint64_t)cards[par[np]];
+    ++np;
+  }
+  const int cv = cards[v];
+  for (uint64_t cell = threadIdx.x; cell < r * cv; cell += blockDim.x) {
+    const uint64_t cfg = cell / cv;
+    const int x = (int)(cell - cfg * cv);
+    uint32_t total = 0;
+    for (int w = 0; w < W; ++w) {
+      uint32_t word = (w == W - 1) ? last_mask : 0xFFFFFFFFu;
+      uint64_t rem = cfg;
+      for (int j = 0; j < np; ++j) {
+        const int cj = cards[par[j]];
+        word &= bits[boff[par[j]] + (uint32_t)(rem % cj) * W + w];
+        rem /= cj;
+      }
+      word &= bits[boff[v] + (uint32_t)x * W + w];
+      total += __popc(word);
+    }
+    out[offsets[e] + cell] = total;
+  }
+}
+
+}  // namespace bnmc_dev
+
+namespace bnmc_host {
+
+struct Bitplanes {
+  uint32_t* bits = nullptr;
+  uint32_t* boff = nullptr;
+  int* cards = nullptr;
+  int W = 0;
+  uint32_t last_mask = 0;
+  ~Bitplanes() {
+    if (bits) cudaFree(bits);
+    if (boff) cudaFree(boff);
+    if (cards) cudaFree(cards);
+  }
+};
+
+inline void make_bitplanes(Bitplanes& bp, const uint8_t* cells, const int* cards, uint64_t m,
+                           int n, cudaStream_t stream) {
+  bp.W = static_cast<int>((m + 31) / 32);
+  const int rem = static_cast<int>(m % 32);
+  bp.last_mask = rem ? ((1u << rem) - 1u) : 0xFFFFFFFFu;
+  std::vector<uint32_t> boff(n);
+  uint64_t words = 0;
+  for (int i = 0; i < n; ++i) {
+    boff[i] = static_cast<uint32_t>(words);
+    words += static_cast<uint64_t>(cards[i]) * bp.W;
+  }
+  if (words > 0xFFFFFFFFull) raise(BNMC_CAPACITY, "sample bitplanes exceed 2^32 words");
+  CK(cudaMalloc(&bp.bits, std::max<uint64_t>(words, 1) * 4));
+  CK(cudaMalloc(&bp.boff, sizeof(uint32_t) * n));
+  CK(cudaMalloc(&bp.cards, sizeof(int) * n));
+  CK(cudaMemcpyAsync(bp.boff, boff.data(), sizeof(uint32_t) * n, cudaMemcpyHostToDevice, stream));
+  CK(cudaMemcpyAsync(bp.cards, cards, sizeof(int) * n, cudaMemcpyHostToDevice, stream));
+  if (m > 0) {
+    uint8_t* d_cells = nullptr;
+    CK(cudaMalloc(&d_cells, m * n));
+    CK(cudaMemcpyAsync(d_cells, cells, m * n, cudaMemcpyHostToDevice, stream));
+    bnmc_dev::bitplane_kernel<<<dim3((bp.W + 127) / 128, n), 128, 0, stream>>>(
+        d_cells, bp.cards, bp.boff, bp.bits, n, m, bp.W);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(stream));
+    cudaFree(d_cells);
+  }
+}
+
+// Distinct parent-configuration counts r = product of <= s cardinalities
+// (bounded by the dense limit), by recursion over distinct card values.
+inline void products(const std::vector<std::pair<int, int>>& cm, size_t i, int left, uint64_t r,
+                     std::set<uint64_t>& out) {
+  out.insert(r);
+  if (left == 0) return;
+  for (size_t j = i; j < cm.size(); ++j) {
+    uint64_t rr = r;
+    for (int e = 1; e <= std::min(left, cm[j].second); ++e) {
+      rr *= static_cast<uint64_t>(cm[j].first);
+      if (rr > static_cast<uint64_t>(bnmc_dev::kHMax)) break;
+      products(cm, j + 1, left - e, rr, out);
+    }
+  }
+}
+
+inline void precompute_rows(cudaStream_t stream, double* d_ls, uint64_t S, const uint8_t* cells,
+                            const int* cards, uint64_t m, int n, int s, double gamma, double ess,
+                            int alpha, int row_begin, int row_end, float* ms_out) {
+  using namespace bnmc_dev;
+  // Dense-counter bounds: largest joint set U (s+1 members) and prefix P (s).
+  std::vector<int> sorted(cards, cards + n);
+  std::sort(sorted.rbegin(), sorted.rend());
+  uint64_t hu = 1, hp = 1;
+  for (int i = 0; i < std::min(n, s + 1); ++i) hu *= sorted[i];
+  for (int i = 0; i < std::min(n, s); ++i) hp *= sorted[i];
+  if (hu > static_cast<uint64_t>(kHMax) || hp > static_cast<uint64_t>(kRPMax))
+    raise(BNMC_CAPACITY, "joint configuration space of up to s+1 variables (" + std::to_string(hu) +
+                             " cells) exceeds the device dense counter (" +
+                             std::to_string(kHMax) + ")");
+  const int cmax = sorted[0];
+
+  Bitplanes bp;
+  make_bitplanes(bp, cells, cards, m, n, stream);
+
+  // LUT pairs (r, card) and glibc lgamma values (log10_gamma, scoring.hpp:16-18).
+  std::vector<std::pair<int, int>> cm;
+  for (int i = 0; i < n;) {
+    int j = i;
+    while (j < n && sorted[j] == sorted[i]) ++j;
+    cm.push_back({sorted[i], j - i});
+    i = j;
+  }
+  std::set<uint64_t> prods;
+  products(cm, 0, s, 1, prods);
+  std::vector<uint64_t> keys;
+  for (uint64_t r : prods)
+    for (auto& c : cm)
+      if (r * c.first <= static_cast<uint64_t>(kHMax)) keys.push_back(r * 512 + c.first);
+  std::sort(keys.begin(), keys.end());
+  const uint64_t stride = 2 * (m + 1);
+  if (keys.size() * stride * 8 > (uint64_t(2) << 30))
+    raise(BNMC_CAPACITY, "lgamma lookup tables would exceed 2 GiB");
+  std::vector<double> lut(keys.size() * stride);
+  const double K = 0.43429448190325182765;  // 1/ln(10), scoring.hpp:17
+  for (size_t p = 0; p < keys.size(); ++p) {
+    const uint64_t r = keys[p] / 512;
+    const int card = static_cast<int>(keys[p] % 512);
+    // Hyperparams::alpha_cell (scoring.hpp:27-31); a_row (scoring.cpp:116)
+    const double a_cell = alpha == BNMC_ALPHA_BDEU ? ess / (static_cast<double>(r) * card) : 1.0;
+    if (!(a_cell > 0.0)) raise(BNMC_USAGE, "Dirichlet hyperparameter must be positive");
+    const double a_row = a_cell * card;
+    double* o = lut.data() + p * stride;
+    for (uint64_t c = 0; c <= m; ++c) {
+      const uint32_t cc = static_cast<uint32_t>(c);
+      o[c] = std::lgamma(cc + a_cell) * K;
+      o[m + 1 + c] = std::lgamma(a_row + cc) * K;
+    }
+  }
+  uint64_t* d_keys = nullptr;
+  double* d_lut = nullptr;
+  int* d_err = nullptr;
+  CK(cudaMalloc(&d_keys, std::max<size_t>(1, keys.size()) * 8));
+  CK(cudaMalloc(&d_lut, std::max<size_t>(1, lut.size()) * 8));
+  CK(cudaMalloc(&d_err, sizeof(int)));
+  CK(cudaMemcpyAsync(d_keys, keys.data(), keys.size() * 8, cudaMemcpyHostToDevice, stream));
+  CK(cudaMemcpyAsync(d_lut, lut.data(), lut.size() * 8, cudaMemcpyHostToDevice, stream));
+  CK(cudaMemsetAsync(d_err, 0, sizeof(int), stream));
+
+  K1Args a{};
+  a.bits = bp.bits;
+  a.boff = bp.boff;
+  a.cards = bp.cards;
+  a.n = n;
+  a.s = s;
+  a.W = bp.W;
+  a.last_mask = bp.last_mask;
+  a.cmax = cmax;
+  a.pair_keys = d_keys;
+  a.n_pairs = static_cast<int>(keys.size());
+  a.lut = d_lut;
+  a.lut_stride = stride;
+  a.m = m;
+  a.log10_gamma = std::log10(gamma);
+  a.ls = d_ls;
+  a.S = S;
+  a.row_begin = row_begin;
+  a.row_end = row_end;
+  // Shared memory: PB tile + NP + CNT for a group of extensions.
+  const size_t budget = 200 * 1024;
+  const int rPmax = static_cast<int>(hp);
+  a.EG = std::max(1, std::min(n, static_cast<int>((64 * 1024) / (4ull * rPmax * cmax))));
+  const size_t cnt_bytes = 4ull * a.EG * rPmax * cmax + 4ull * rPmax;
+  a.WT = std::max(1, std::min(std::max(bp.W, 1), static_cast<int>((budget - cnt_bytes) / (4ull * rPmax))));
+  a.error = d_err;
+  const size_t shm = 4ull * rPmax * a.WT + cnt_bytes;
+  CK(cudaFuncSetAttribute(k1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          static_cast<int>(shm)));
+  const uint64_t prefixes = [&] {
+    uint64_t t = 0;
+    for (int j = 0; j <= std::min(s, n); ++j) {
+      uint64_t c = 1;
+      for (int i = 0; i < j; ++i) c = c * (n - i) / (i + 1);
+      t += c;
+    }
+    return t;
+  }();
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  CK(cudaEventRecord(e0, stream));
+  const uint64_t chunk = 1u << 30;
+  for (uint64_t base = 0; base < prefixes; base += chunk) {
+    const unsigned blocks = static_cast<unsigned>(std::min(chunk, prefixes - base));
+    k1_kernel<<<blocks, kK1Threads, shm, stream>>>(a, base);
+    CK(cudaGetLastError());
+  }
+  CK(cudaEventRecord(e1, stream));
+  CK(cudaEventSynchronize(e1));
+  CK(cudaEventElapsedTime(ms_out, e0, e1));
+  int err = 0;
+  CK(cudaMemcpy(&err, d_err, sizeof(int), cudaMemcpyDeviceToHost));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(d_keys);
+  cudaFree(d_lut);
+  cudaFree(d_err);
+  if (err) raise(BNMC_ERR, "precompute kernel reported internal error " + std::to_string(err));
+}
+
+inline void count_statistics_device(const uint8_t* cells, const int* cards, uint64_t m, int n,
+                                    int count, const int* nodes, const uint64_t* psets,
+                                    const uint64_t* offsets, uint32_t* out, uint64_t* configs_out) {
+  if (n < 1 || n > 64) raise(BNMC_DATA, "dataset must have between 1 and 64 variables");
+  uint64_t total = 0;
+  for (int e = 0; e < count; ++e) {
+    if (nodes[e] < 0 || nodes[e] >= n) raise(BNMC_USAGE, "node out of range");
+    if ((psets[e] >> nodes[e]) & 1u) raise(BNMC_DATA, "node cannot appear in its own parent set");
+    if (n < 64 && (psets[e] >> n)) raise(BNMC_USAGE, "parent out of range");
+    uint64_t r = 1;
+    for (uint64_t mm = psets[e]; mm; mm &= mm - 1) {
+      const uint64_t c = static_cast<uint64_t>(cards[__builtin_ctzll(mm)]);
+      if (r > ~0ull / c) raise(BNMC_CAPACITY, "parent configuration space overflows 64 bits");
+      r *= c;
+    }
+    if (r * cards[nodes[e]] > (1ull << 24)) raise(BNMC_CAPACITY, "count table too large");
+    configs_out[e] = r;
+    total = std::max<uint64_t>(total, offsets[e] + r * cards[nodes[e]]);
+  }
+  cudaStream_t stream;
+  CK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+  {
+    Bitplanes bp;
+    make_bitplanes(bp, cells, cards, m, n, stream);
+    int* d_nodes = nullptr;
+    uint64_t *d_psets = nullptr, *d_off = nullptr;
+    uint32_t* d_out = nullptr;
+    CK(cudaMalloc(&d_nodes, sizeof(int) * count));
+    CK(cudaMalloc(&d_psets, 8ull * count));
+    CK(cudaMalloc(&d_off, 8ull * count));
+    CK(cudaMalloc(&d_out, 4ull * std::max<uint64_t>(total, 1)));
+    CK(cudaMemcpyAsync(d_nodes, nodes, sizeof(int) * count, cudaMemcpyHostToDevice, stream));
+    CK(cudaMemcpyAsync(d_psets, psets, 8ull * count, cudaMemcpyHostToDevice, stream));
+    CK(cudaMemcpyAsync(d_off, offsets, 8ull * count, cudaMemcpyHostToDevice, stream));
+    if (bp.W == 0) {
+      CK(cudaMemsetAsync(d_out, 0, 4ull * std::max<uint64_t>(total, 1), stream));
+    } else {
+      bnmc_dev::counts_kernel<<<count, 256, 0, stream>>>(bp.bits, bp.boff, bp.cards, bp.W,
+                                                         bp.last_mask, d_nodes, d_psets, d_off,
+                                                         d_out);
+      CK(cudaGetLastError());
+    }
+    CK(cudaMemcpyAsync(out, d_out, 4ull * total, cudaMemcpyDeviceToHost, stream));
+    CK(cudaStreamSynchronize(stream));
+    cudaFree(d_nodes);
+    cudaFree(d_psets);
+    cudaFree(d_off);
+    cudaFree(d_out);
+  }
+  cudaStreamDestroy(stream);
+}
+
+}  // namespace bnmc_host
