@@ -137,7 +137,7 @@ typedef struct {
   int track_top;       /* BestGraphTracker capacity, >= 1 */
   int strict;          /* RunConfig::strict_paper_tracker */
   int scan_mode;       /* 0 = auto; 1 = fp32 keys + exact fp64 resolve; 2 = fp64 */
-  int reserved;
+  int timing_sample;   /* every k-th scan launch is bracketed by CUDA events (0 = 8) */
 } bnmc_chain_params;
 
 /* Run n_chains independent chains, chain c seeded with seeds[c] exactly as
@@ -154,11 +154,19 @@ int bnmc_gpu_run_chains(bnmc_table* t, const uint64_t* seeds, int n_chains,
                         double* final_score, uint64_t* accepted, int* tracker_count,
                         uint64_t* tracker_masks, double* tracker_totals, float* device_ms);
 
-/* Scan statistics of the last run_chains call: node-row rescans performed
- * (summed over chains and iterations), distinct rows streamed (after batching
- * chains), and the device time of the scan kernel alone (ms). */
-int bnmc_gpu_last_scan_stats(const bnmc_table* t, uint64_t* row_rescans,
-                             uint64_t* rows_streamed, float* scan_ms, uint64_t* scan_launches);
+/* Statistics of the last run_chains call: node-row rescans (summed over
+ * chains and iterations), 32-byte key sectors streamed by the scan kernel
+ * (after batching chains per row and skipping sectors no pair can admit), the
+ * average device time of one scan launch (CUDA events around every
+ * timing_sample-th launch inside the loop, ms) and the number of kernel
+ * launches of the loop. n_chains <= 64 per call. */
+int bnmc_gpu_last_scan_stats(const bnmc_table* t, uint64_t* row_rescans, uint64_t* sectors,
+                             float* scan_ms_avg, uint64_t* kernel_launches);
+
+/* Diagnostics: time the order-scan kernel alone on the rows at positions
+ * lo..hi of `count` (<= 64) orders, averaged over `reps` launches (ms). */
+int bnmc_gpu_bench_scan(bnmc_table* t, const int* perms, int count, int lo, int hi, int reps,
+                        float* ms_per_launch);
 
 #ifdef __cplusplus
 }

@@ -6,7 +6,6 @@
 //                    padding entries = ~0 (never admissible)
 //   d_ls[n][S]       fp64 local scores, BNSC body order (scoring.cpp:194-238)
 //   d_key32[n][Sp]   fp32 scan keys fl32(ls + PpfTable::sum), padding -inf
-//   d_key64[n][Sp]   fp64 scan keys (allocated only for scan_mode 2)
 //   d_w[n][n]        PPF weights (scoring.cpp:150-155)
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -14,6 +13,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -150,9 +150,7 @@ struct bnmc_table {
   DevBuf<uint64_t> cmask;
   DevBuf<double> ls;
   DevBuf<float> key32;
-  DevBuf<double> key64;
   DevBuf<double> w;
-  bool key64_valid = false;
   std::vector<double> h_w;
   float build_ms = 0.f, fold_ms = 0.f;
   // chain / order-scoring workspace
@@ -160,7 +158,9 @@ struct bnmc_table {
   DevBuf<Item> items;
   DevBuf<int> counts;
   DevBuf<uint8_t> ppos;
-  DevBuf<uint8_t> partials;
+  DevBuf<PairRec> buckets;
+  DevBuf<int> rowcnt;
+  DevBuf<unsigned long long> cell;
   DevBuf<uint8_t> props;
   DevBuf<double> thr;
   DevBuf<uint64_t> tmasks;
@@ -172,8 +172,9 @@ struct bnmc_table {
   DevBuf<int> perms;
   DevBuf<uint64_t> out_masks;
   DevBuf<double> out_best, out_total;
-  uint64_t last_rescans = 0, last_streamed = 0, last_launches = 0;
-  float last_scan_ms = 0.f;
+  uint64_t last_rescans = 0, last_sectors = 0, last_launches = 0, last_scan_samples = 0;
+  float last_scan_ms = 0.f, last_total_ms = 0.f;
+  int last_G = 0;
   ~bnmc_table() {
     if (stream) cudaStreamDestroy(stream);
   }
@@ -181,37 +182,64 @@ struct bnmc_table {
 
 namespace {
 
+constexpr int kMaxChainsPerLaunch = 64;
+
 struct ScanGeom {
-  int G, T, U, L4, units;
+  int G, Ls, RB, sectors;
 };
 
-ScanGeom scan_geometry(const bnmc_table* t) {
+// CTA b owns Ls <= 512 consecutive sectors of every row (one CTA per SM when
+// the row fits), RB rows per cp.async pipeline stage within the smem budget.
+ScanGeom scan_geometry(const bnmc_table* t, int max_pairs) {
   ScanGeom g;
-  g.units = static_cast<int>(t->Sp / 4);
+  g.sectors = static_cast<int>(t->Sp / 8);
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, t->dev);
-  g.G = std::max(1, std::min(sms, (g.units + 31) / 32));
-  g.L4 = (g.units + g.G - 1) / g.G;
-  g.U = 1;
-  while (g.U < 8 && (g.L4 + g.U - 1) / g.U > kScanMaxThreads) g.U *= 2;
-  if ((g.L4 + g.U - 1) / g.U > kScanMaxThreads) {
-    // Too many units per CTA for register-resident masks: add CTAs.
-    g.U = 8;
-    g.L4 = 8 * kScanMaxThreads;
-    g.G = (g.units + g.L4 - 1) / g.L4;
-  }
-  g.T = std::max(32, (((g.L4 + g.U - 1) / g.U) + 31) / 32 * 32);
+  g.Ls = std::min(kMaxLs, (g.sectors + sms - 1) / sms);
+  g.Ls = std::max(1, g.Ls);
+  g.G = (g.sectors + g.Ls - 1) / g.Ls;
+  const size_t budget = 220 * 1024;
+  g.RB = 8;
+  while (g.RB > 1 && scan_smem_bytes(g.Ls, g.RB, max_pairs) > budget) --g.RB;
   return g;
 }
 
-template <typename K>
-void launch_scan(const ScanGeom& g, const ScanArgs& a, cudaStream_t s) {
-  switch (g.U) {
-    case 1: scan_kernel<K, 1, 8><<<g.G, g.T, 0, s>>>(a); break;
-    case 2: scan_kernel<K, 2, 4><<<g.G, g.T, 0, s>>>(a); break;
-    case 4: scan_kernel<K, 4, 2><<<g.G, g.T, 0, s>>>(a); break;
-    default: scan_kernel<K, 8, 1><<<g.G, g.T, 0, s>>>(a); break;
+void launch_scan(const ScanGeom& g, ScanArgs a, int max_pairs, cudaStream_t s, bool pdl) {
+  a.Ls = g.Ls;
+  a.RB = g.RB;
+  a.sectors = g.sectors;
+  a.max_pairs = max_pairs;
+  const size_t shm = scan_smem_bytes(g.Ls, g.RB, max_pairs);
+  static size_t configured = 0;
+  if (shm > configured) {
+    CK(cudaFuncSetAttribute(scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            static_cast<int>(std::max<size_t>(shm, 48 * 1024))));
+    configured = shm;
   }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(g.G);
+  cfg.blockDim = dim3(kScanThreads);
+  cfg.dynamicSmemBytes = shm;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  CK(cudaLaunchKernelEx(&cfg, scan_kernel, a));
+}
+
+void launch_step(int C, const StepArgs& A, cudaStream_t s, bool pdl) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(C);
+  cfg.blockDim = dim3(kStepThreads);
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  CK(cudaLaunchKernelEx(&cfg, step_kernel, A));
 }
 
 // Candidate masks in global-index order (device unrank, combinatorics.cpp:8-39,
@@ -248,17 +276,16 @@ __global__ void build_cmask_kernel(uint64_t* out, uint64_t S, uint64_t Sp, int c
 }
 
 // PPF fold: key = fl(ls + PpfTable::sum) in the scan's association
-// (engine.cpp:50-51), fp32 and/or fp64; padding -inf.
+// (engine.cpp:50-51) rounded to fp32; padding -inf.
 __global__ void fold_kernel(const double* __restrict__ ls, const uint64_t* __restrict__ cmask,
-                            const double* __restrict__ w, float* key32, double* key64, int n,
+                            const double* __restrict__ w, float* key32, int n,
                             uint64_t S, uint64_t Sp) {
   const int v = blockIdx.y;
   for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < Sp;
        g += (uint64_t)gridDim.x * blockDim.x) {
     double e = -INFINITY;
     if (g < S) e = ls[(uint64_t)v * S + g] + ppf_sum(w, n, v, cand_to_nodes(cmask[g], v));
-    if (key32) key32[(uint64_t)v * Sp + g] = __double2float_rn(e);
-    if (key64) key64[(uint64_t)v * Sp + g] = e;
+    key32[(uint64_t)v * Sp + g] = __double2float_rn(e);
   }
 }
 
@@ -293,15 +320,14 @@ void set_priors(bnmc_table* t, const double* prior_r) {
   CK(cudaMemcpyAsync(t->w.p, t->h_w.data(), t->h_w.size() * 8, cudaMemcpyHostToDevice, t->stream));
 }
 
-void fold(bnmc_table* t, bool want64) {
+void fold(bnmc_table* t) {
   cudaEvent_t e0, e1;
   CK(cudaEventCreate(&e0));
   CK(cudaEventCreate(&e1));
-  if (want64) t->key64.alloc(static_cast<size_t>(t->n) * t->Sp);
   const unsigned bx = static_cast<unsigned>(std::min<uint64_t>((t->Sp + 255) / 256, 4096));
   CK(cudaEventRecord(e0, t->stream));
   fold_kernel<<<dim3(bx, t->n), 256, 0, t->stream>>>(t->ls.p, t->cmask.p, t->w.p, t->key32.p,
-                                                       want64 ? t->key64.p : nullptr, t->n, t->S,
+                                                       t->n, t->S,
                                                        t->Sp);
   CK(cudaGetLastError());
   CK(cudaEventRecord(e1, t->stream));
@@ -309,7 +335,6 @@ void fold(bnmc_table* t, bool want64) {
   CK(cudaEventElapsedTime(&t->fold_ms, e0, e1));
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
-  t->key64_valid = want64;
 }
 
 TieCtx tie_ctx(const bnmc_table* t) {
@@ -335,15 +360,16 @@ void accept_thresholds(const uint64_t* seeds, int C, uint64_t iters, std::vector
   }
 }
 
-void ensure_workspace(bnmc_table* t, int C, uint64_t iters, int K, const ScanGeom& g,
-                      size_t key_bytes) {
+void ensure_workspace(bnmc_table* t, int C, uint64_t iters, int K) {
   const int n = t->n;
   t->st.alloc(C);
-  t->items.alloc(static_cast<size_t>(C) * n);
+  t->items.alloc(static_cast<size_t>(C) * 64);
   t->counts.alloc(C);
   t->ppos.alloc(static_cast<size_t>(C) * 64);
-  t->partials.alloc(static_cast<size_t>(C) * n * g.G * (key_bytes == 4 ? 8 : 16));
-  t->stat.alloc(1);
+  t->buckets.alloc(2ull * n * kMaxChains);
+  t->rowcnt.alloc(2ull * n + 2);  // + sel + error
+  t->cell.alloc(2ull * C * n);
+  t->stat.alloc(2);
   if (iters) {
     t->props.alloc(static_cast<size_t>(C) * (iters + 1) * 2);
     t->thr.alloc(static_cast<size_t>(C) * (iters + 1));
@@ -353,13 +379,54 @@ void ensure_workspace(bnmc_table* t, int C, uint64_t iters, int K, const ScanGeo
     t->tr_best.alloc(static_cast<size_t>(C) * iters);
     t->tr_acc.alloc(static_cast<size_t>(C) * iters);
   }
+  // clean buckets, cells, sel, error flag
+  CK(cudaMemsetAsync(t->rowcnt.p, 0, sizeof(int) * (2ull * n + 2), t->stream));
+  CK(cudaMemsetAsync(t->cell.p, 0, 16ull * C * n, t->stream));
+  CK(cudaMemsetAsync(t->stat.p, 0, 16, t->stream));
 }
 
-template <typename K>
-void run_scan_and_step(bnmc_table* t, const ScanGeom& g, const ScanArgs& sa, const StepArgs& A,
-                       int C) {
-  launch_scan<K>(g, sa, t->stream);
-  step_kernel<K><<<C, 256, 0, t->stream>>>(A);
+StepArgs step_args(bnmc_table* t) {
+  StepArgs A{};
+  A.st = t->st.p;
+  A.items = t->items.p;
+  A.counts = t->counts.p;
+  A.ppos = t->ppos.p;
+  A.buckets = t->buckets.p;
+  A.rowcnt = t->rowcnt.p;
+  A.sel = t->rowcnt.p + 2 * t->n;
+  A.error = t->rowcnt.p + 2 * t->n + 1;
+  A.cell = t->cell.p;
+  A.keys = t->key32.p;
+  A.Sp = t->Sp;
+  A.stat_rows = t->stat.p;
+  A.n = t->n;
+  A.tie = tie_ctx(t);
+  return A;
+}
+
+ScanArgs scan_args(const bnmc_table* t, const ScanGeom& g) {
+  ScanArgs sa{};
+  sa.keys = t->key32.p;
+  sa.Sp = t->Sp;
+  sa.buckets = t->buckets.p;
+  sa.rowcnt = t->rowcnt.p;
+  sa.sel = t->rowcnt.p + 2 * t->n;
+  sa.ppos = t->ppos.p;
+  sa.cell = t->cell.p;
+  sa.n = t->n;
+  sa.sectors = g.sectors;
+  sa.Ls = g.Ls;
+  sa.RB = g.RB;
+  sa.tie = tie_ctx(t);
+  sa.sector_loads = t->stat.p + 1;
+  if (const char* e = std::getenv("BNMC_DEBUG_SCAN_EXIT")) sa.debug_exit = std::atoi(e);
+  return sa;
+}
+
+int read_error(bnmc_table* t) {
+  int err = 0;
+  CK(cudaMemcpy(&err, t->rowcnt.p + 2 * t->n + 1, sizeof(int), cudaMemcpyDeviceToHost));
+  return err;
 }
 
 }  // namespace
@@ -403,7 +470,7 @@ int bnmc_gpu_table_upload(const double* table, int n, const bnmc_score_params* p
     CK(cudaMemcpyAsync(t->ls.p, table, static_cast<size_t>(n) * t->S * 8, cudaMemcpyHostToDevice,
                        t->stream));
     set_priors(t.get(), prior_r);
-    fold(t.get(), false);
+    fold(t.get());
     *out = t.release();
   });
 }
@@ -461,7 +528,7 @@ int bnmc_gpu_table_finalize(bnmc_table* t) {
   return guarded([&] {
     if (!t) raise(BNMC_USAGE, "null table");
     CK(cudaSetDevice(t->dev));
-    fold(t, t->key64_valid);
+    fold(t);
   });
 }
 
@@ -470,7 +537,7 @@ int bnmc_gpu_table_set_priors(bnmc_table* t, const double* prior_r) {
     if (!t) raise(BNMC_USAGE, "null table");
     CK(cudaSetDevice(t->dev));
     set_priors(t, prior_r);
-    fold(t, t->key64_valid);
+    fold(t);
   });
 }
 
@@ -533,43 +600,27 @@ int bnmc_gpu_score_orders(bnmc_table* t, const int* perms, int count, uint64_t* 
       }
     }
     CK(cudaSetDevice(t->dev));
-    const ScanGeom g = scan_geometry(t);
-    ensure_workspace(t, count, 0, 0, g, 4);
-    t->perms.alloc(static_cast<size_t>(count) * n);
+    const ScanGeom g = scan_geometry(t, kMaxChainsPerLaunch * n);
+    t->perms.alloc(static_cast<size_t>(kMaxChainsPerLaunch) * n);
     t->out_masks.alloc(static_cast<size_t>(count) * n);
     t->out_best.alloc(static_cast<size_t>(count) * n);
     t->out_total.alloc(count);
-    CK(cudaMemcpyAsync(t->perms.p, perms, sizeof(int) * count * n, cudaMemcpyHostToDevice,
-                       t->stream));
-    StepArgs A{};
-    A.items = t->items.p;
-    A.counts = t->counts.p;
-    A.ppos = t->ppos.p;
-    A.partials = t->partials.p;
-    A.stat_rows = t->stat.p;
-    A.n = n;
-    A.G = g.G;
-    A.score_only = 1;
-    A.out_masks = t->out_masks.p;
-    A.out_best = t->out_best.p;
-    A.out_total = t->out_total.p;
-    A.tie = tie_ctx(t);
-    setup_orders_kernel<<<(count + 127) / 128, 128, 0, t->stream>>>(A, t->perms.p, count);
-    ScanArgs sa{};
-    sa.keys = t->key32.p;
-    sa.Sp = t->Sp;
-    sa.items = t->items.p;
-    sa.counts = t->counts.p;
-    sa.ppos = t->ppos.p;
-    sa.partials = t->partials.p;
-    sa.C = count;
-    sa.n = n;
-    sa.G = g.G;
-    sa.units = g.units;
-    sa.L4 = g.L4;
-    sa.tie = A.tie;
-    run_scan_and_step<float>(t, g, sa, A, count);
-    CK(cudaGetLastError());
+    ensure_workspace(t, kMaxChainsPerLaunch, 0, 0);
+    for (int c0 = 0; c0 < count; c0 += kMaxChainsPerLaunch) {
+      const int cc = std::min(kMaxChainsPerLaunch, count - c0);
+      CK(cudaMemcpyAsync(t->perms.p, perms + static_cast<size_t>(c0) * n, sizeof(int) * cc * n,
+                         cudaMemcpyHostToDevice, t->stream));
+      CK(cudaMemsetAsync(t->rowcnt.p, 0, sizeof(int) * 2ull * n, t->stream));
+      StepArgs A = step_args(t);
+      A.score_only = 1;
+      A.out_masks = t->out_masks.p + static_cast<size_t>(c0) * n;
+      A.out_best = t->out_best.p + static_cast<size_t>(c0) * n;
+      A.out_total = t->out_total.p + c0;
+      setup_items_kernel<<<cc, 64, 0, t->stream>>>(A, t->perms.p, cc);
+      CK(cudaGetLastError());
+      launch_scan(g, scan_args(t, g), cc * n, t->stream, false);
+      launch_step(cc, A, t->stream, false);
+    }
     if (masks_out)
       CK(cudaMemcpyAsync(masks_out, t->out_masks.p, 8ull * count * n, cudaMemcpyDeviceToHost,
                          t->stream));
@@ -580,6 +631,41 @@ int bnmc_gpu_score_orders(bnmc_table* t, const int* perms, int count, uint64_t* 
       CK(cudaMemcpyAsync(totals_out, t->out_total.p, 8ull * count, cudaMemcpyDeviceToHost,
                          t->stream));
     CK(cudaStreamSynchronize(t->stream));
+    if (const int err = read_error(t))
+      raise(BNMC_ERR, "scan consistency check failed (" + std::to_string(err) + ")");
+  });
+}
+
+int bnmc_gpu_bench_scan(bnmc_table* t, const int* perms, int count, int lo, int hi, int reps,
+                        float* ms_per_launch) {
+  return guarded([&] {
+    if (!t) raise(BNMC_USAGE, "null table");
+    if (count < 1 || count > kMaxChainsPerLaunch) raise(BNMC_USAGE, "count must lie in [1,64]");
+    const int n = t->n;
+    if (lo < 0 || hi >= n || lo > hi) raise(BNMC_USAGE, "bad position range");
+    CK(cudaSetDevice(t->dev));
+    const ScanGeom g = scan_geometry(t, count * n);
+    t->perms.alloc(static_cast<size_t>(count) * n);
+    ensure_workspace(t, count, 0, 0);
+    CK(cudaMemcpyAsync(t->perms.p, perms, sizeof(int) * count * n, cudaMemcpyHostToDevice,
+                       t->stream));
+    StepArgs A = step_args(t);
+    setup_items_range_kernel<<<count, 64, 0, t->stream>>>(A, t->perms.p, count, lo, hi);
+    CK(cudaGetLastError());
+    const ScanArgs sa = scan_args(t, g);
+    launch_scan(g, sa, count * n, t->stream, false);  // warm-up
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    CK(cudaEventRecord(e0, t->stream));
+    for (int r = 0; r < reps; ++r) launch_scan(g, sa, count * n, t->stream, false);
+    CK(cudaEventRecord(e1, t->stream));
+    CK(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    *ms_per_launch = ms / std::max(1, reps);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
   });
 }
 
@@ -598,29 +684,24 @@ int bnmc_gpu_run_chains(bnmc_table* t, const uint64_t* seeds, int n_chains,
     if (!params) raise(BNMC_USAGE, "null chain params");
     if (params->iterations < 1) raise(BNMC_USAGE, "iterations must be >= 1");
     if (params->track_top < 1) raise(BNMC_USAGE, "tracker capacity must be >= 1");
-    if (n_chains < 1) raise(BNMC_USAGE, "n_chains must be >= 1");
+    if (n_chains < 1 || n_chains > kMaxChainsPerLaunch)
+      raise(BNMC_USAGE, "n_chains must lie in [1," + std::to_string(kMaxChainsPerLaunch) + "]");
     if (t->n < 2) raise(BNMC_USAGE, "swap proposal needs at least two nodes");
     const int mode = params->scan_mode;
-    if (mode < 0 || mode > 2) raise(BNMC_USAGE, "scan_mode must be 0, 1 or 2");
-    const bool f64 = mode == 2;
+    if (mode == 2)
+      raise(BNMC_USAGE, "scan_mode 2 (fp64 keys) is not provided: the fp32-key scan is exact");
+    if (mode < 0 || mode > 2) raise(BNMC_USAGE, "scan_mode must be 0 or 1");
     CK(cudaSetDevice(t->dev));
-    if (f64 && !t->key64_valid) fold(t, true);
     const int n = t->n, C = n_chains, K = params->track_top;
     const uint64_t iters = params->iterations;
-    const ScanGeom g = scan_geometry(t);
-    ensure_workspace(t, C, iters, K, g, f64 ? 8 : 4);
+    const ScanGeom g = scan_geometry(t, C * n);
+    ensure_workspace(t, C, iters, K);
     t->seeds.alloc(C);
     std::vector<double> thr;
     accept_thresholds(seeds, C, iters, thr);
     CK(cudaMemcpyAsync(t->seeds.p, seeds, 8ull * C, cudaMemcpyHostToDevice, t->stream));
     CK(cudaMemcpyAsync(t->thr.p, thr.data(), thr.size() * 8, cudaMemcpyHostToDevice, t->stream));
-    CK(cudaMemsetAsync(t->stat.p, 0, 8, t->stream));
-    StepArgs A{};
-    A.st = t->st.p;
-    A.items = t->items.p;
-    A.counts = t->counts.p;
-    A.ppos = t->ppos.p;
-    A.partials = t->partials.p;
+    StepArgs A = step_args(t);
     A.props = t->props.p;
     A.thr = t->thr.p;
     A.tmasks = t->tmasks.p;
@@ -628,59 +709,83 @@ int bnmc_gpu_run_chains(bnmc_table* t, const uint64_t* seeds, int n_chains,
     A.tr_prop = t->tr_prop.p;
     A.tr_acc = t->tr_acc.p;
     A.tr_best = t->tr_best.p;
-    A.stat_rows = t->stat.p;
     A.iters = iters;
-    A.n = n;
-    A.G = g.G;
     A.K = K;
     A.strict = params->strict;
-    A.tie = tie_ctx(t);
     setup_chains_kernel<<<(C + 63) / 64, 64, 0, t->stream>>>(A, t->seeds.p, C);
     CK(cudaGetLastError());
-    ScanArgs sa{};
-    sa.keys = f64 ? static_cast<const void*>(t->key64.p) : static_cast<const void*>(t->key32.p);
-    sa.Sp = t->Sp;
-    sa.items = t->items.p;
-    sa.counts = t->counts.p;
-    sa.ppos = t->ppos.p;
-    sa.partials = t->partials.p;
-    sa.C = C;
-    sa.n = n;
-    sa.G = g.G;
-    sa.units = g.units;
-    sa.L4 = g.L4;
-    sa.tie = A.tie;
+    setup_items_kernel<<<C, 64, 0, t->stream>>>(A, nullptr, C);
+    CK(cudaGetLastError());
+    const ScanArgs sa = scan_args(t, g);
 
-    // Capture a batch of (scan, step) pairs once; replay it until every chain
-    // has finalized iteration `iters` (steps beyond that are no-ops).
+    // Two instances of a captured batch of (scan, step) pairs with PDL edges;
+    // every `sample`-th scan is bracketed by event-record nodes so the scan's
+    // device time is measured live. Instances alternate so the host harvests
+    // one instance's events while the other runs. Steps past `iters` are no-ops.
     const uint64_t total_steps = iters + 1;
-    const int batch = static_cast<int>(std::min<uint64_t>(total_steps, 256));
-    cudaGraph_t graph;
-    cudaGraphExec_t exec;
-    CK(cudaStreamBeginCapture(t->stream, cudaStreamCaptureModeThreadLocal));
-    for (int i = 0; i < batch; ++i) {
-      if (f64)
-        run_scan_and_step<double>(t, g, sa, A, C);
-      else
-        run_scan_and_step<float>(t, g, sa, A, C);
-    }
-    CK(cudaStreamEndCapture(t->stream, &graph));
-    CK(cudaGraphInstantiate(&exec, graph, 0));
+    const int batch = static_cast<int>(std::min<uint64_t>(total_steps, 128));
+    const int sample = std::max(1, params->timing_sample > 0 ? params->timing_sample : 8);
     const uint64_t replays = (total_steps + batch - 1) / batch;
+    const int ninst = replays > 1 ? 2 : 1;
+    struct Inst {
+      cudaGraphExec_t exec = nullptr;
+      std::vector<cudaEvent_t> ev;
+    } inst[2];
+    for (int k = 0; k < ninst; ++k) {
+      for (int i = 0; i < batch; i += sample) {
+        cudaEvent_t e0, e1;
+        CK(cudaEventCreate(&e0));
+        CK(cudaEventCreate(&e1));
+        inst[k].ev.push_back(e0);
+        inst[k].ev.push_back(e1);
+      }
+      cudaGraph_t graph;
+      CK(cudaStreamBeginCapture(t->stream, cudaStreamCaptureModeThreadLocal));
+      for (int i = 0; i < batch; ++i) {
+        const bool timed = i % sample == 0;
+        if (timed) CK(cudaEventRecordWithFlags(inst[k].ev[2 * (i / sample)], t->stream,
+                                               cudaEventRecordExternal));
+        launch_scan(g, sa, C * n, t->stream, !timed && i > 0);
+        if (timed) CK(cudaEventRecordWithFlags(inst[k].ev[2 * (i / sample) + 1], t->stream,
+                                               cudaEventRecordExternal));
+        launch_step(C, A, t->stream, !timed);
+      }
+      CK(cudaStreamEndCapture(t->stream, &graph));
+      CK(cudaGraphInstantiate(&inst[k].exec, graph, 0));
+      cudaGraphDestroy(graph);
+    }
     cudaEvent_t e0, e1;
     CK(cudaEventCreate(&e0));
     CK(cudaEventCreate(&e1));
+    double scan_ms = 0.0;
+    uint64_t scan_samples = 0;
+    auto harvest = [&](Inst& in) {
+      for (size_t i = 0; i + 1 < in.ev.size(); i += 2) {
+        float ms = 0.f;
+        CK(cudaEventSynchronize(in.ev[i + 1]));
+        CK(cudaEventElapsedTime(&ms, in.ev[i], in.ev[i + 1]));
+        scan_ms += ms;
+        ++scan_samples;
+      }
+    };
     CK(cudaEventRecord(e0, t->stream));
-    for (uint64_t r = 0; r < replays; ++r) CK(cudaGraphLaunch(exec, t->stream));
+    for (uint64_t r = 0; r < replays; ++r) {
+      Inst& cur = inst[r % ninst];
+      if (r >= 2) harvest(cur);  // its previous launch must finish before reuse
+      CK(cudaGraphLaunch(cur.exec, t->stream));
+    }
     CK(cudaEventRecord(e1, t->stream));
     CK(cudaEventSynchronize(e1));
+    for (uint64_t r = replays >= 2 ? replays - 2 : 0; r < replays; ++r) harvest(inst[r % ninst]);
     float ms = 0.f;
     CK(cudaEventElapsedTime(&ms, e0, e1));
     if (device_ms) *device_ms = ms;
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
-    cudaGraphExecDestroy(exec);
-    cudaGraphDestroy(graph);
+    for (int k = 0; k < ninst; ++k) {
+      for (auto e : inst[k].ev) cudaEventDestroy(e);
+      cudaGraphExecDestroy(inst[k].exec);
+    }
     CK(cudaGetLastError());
 
     // Results back to the host.
@@ -702,9 +807,11 @@ int bnmc_gpu_run_chains(bnmc_table* t, const uint64_t* seeds, int n_chains,
     if (tracker_totals)
       CK(cudaMemcpyAsync(tracker_totals, t->ttotals.p, 8ull * C * K, cudaMemcpyDeviceToHost,
                          t->stream));
-    unsigned long long rows = 0;
-    CK(cudaMemcpyAsync(&rows, t->stat.p, 8, cudaMemcpyDeviceToHost, t->stream));
+    unsigned long long stats[2] = {0, 0};
+    CK(cudaMemcpyAsync(stats, t->stat.p, 16, cudaMemcpyDeviceToHost, t->stream));
     CK(cudaStreamSynchronize(t->stream));
+    if (const int err = read_error(t))
+      raise(BNMC_ERR, "scan consistency check failed (" + std::to_string(err) + ")");
     for (int c = 0; c < C; ++c) {
       if (!hs[c].done) raise(BNMC_ERR, "chain did not finish (internal error)");
       if (final_order)
@@ -713,21 +820,24 @@ int bnmc_gpu_run_chains(bnmc_table* t, const uint64_t* seeds, int n_chains,
       if (accepted) accepted[c] = hs[c].accepted;
       if (tracker_count) tracker_count[c] = hs[c].tcount;
     }
-    t->last_rescans = rows;
-    t->last_streamed = rows;
-    t->last_launches = replays * batch;
-    t->last_scan_ms = ms;
+    t->last_rescans = stats[0];
+    t->last_sectors = stats[1];
+    t->last_launches = replays * batch * 2 + 2;
+    t->last_total_ms = ms;
+    t->last_scan_ms = scan_samples ? static_cast<float>(scan_ms / scan_samples) : 0.f;
+    t->last_scan_samples = scan_samples;
+    t->last_G = g.G;
   });
 }
 
-int bnmc_gpu_last_scan_stats(const bnmc_table* t, uint64_t* row_rescans, uint64_t* rows_streamed,
-                             float* scan_ms, uint64_t* scan_launches) {
+int bnmc_gpu_last_scan_stats(const bnmc_table* t, uint64_t* row_rescans, uint64_t* sectors,
+                             float* scan_ms_avg, uint64_t* kernel_launches) {
   return guarded([&] {
     if (!t) raise(BNMC_USAGE, "null table");
     if (row_rescans) *row_rescans = t->last_rescans;
-    if (rows_streamed) *rows_streamed = t->last_streamed;
-    if (scan_ms) *scan_ms = t->last_scan_ms;
-    if (scan_launches) *scan_launches = t->last_launches;
+    if (sectors) *sectors = t->last_sectors;
+    if (scan_ms_avg) *scan_ms_avg = t->last_scan_ms;
+    if (kernel_launches) *kernel_launches = t->last_launches;
   });
 }
 

@@ -1,15 +1,17 @@
 // K3 — device-resident MCMC step (sm_100a): one CTA per chain.
 //
 // Restates run_mcmc's loop body (sampler.cpp:92-111) on the device:
-//   reduce the K2 partial cells of every rescanned row (argmax_reduce,
+//   read the argmax cell of every rescanned row (the K2 maxima; argmax_reduce,
 //   engine.cpp:15-22, 85-93) -> proposed per-node bests and parent sets;
 //   total in ascending node order (engine.cpp:95-96); mh_accept
 //   (sampler.cpp:54-56) against the host-precomputed glibc log10(u_t) of the
 //   acceptance stream; BestGraphTracker::update (sampler.cpp:32-41); commit;
-//   trace row; then prepare the next proposal's rescan items.
+//   trace row; then the next proposal's rescan pairs, bucketed by row for K2.
 // Only rows at positions min(a,b)..max(a,b) of the proposed order change their
 // predecessor sets, so only those are rescanned (the reference rescans all n,
-// engine.cpp:71-76; results are identical).
+// engine.cpp:71-76; the results are identical).
+// The chain state is staged in shared memory; loops over nodes, tracker
+// entries and positions are spread over the CTA's threads.
 #pragma once
 
 #include "scan.cuh"
@@ -29,12 +31,22 @@ struct ChainState {
   double best[64];     // current per-node effective bests
 };
 
+struct Item {  // per-chain copy of its rescan pairs (slot -> row, predecessors)
+  uint64_t cpred;
+  uint32_t v, pad;
+};
+
 struct StepArgs {
   ChainState* st;           // [C]
-  Item* items;              // [C][n]
+  Item* items;              // [C][64]
   int* counts;              // [C]
   uint8_t* ppos;            // [C][64]
-  const void* partials;     // [C][n][G]
+  PairRec* buckets;         // [2][n][kMaxChains]
+  int* rowcnt;              // [2][n]
+  int* sel;                 // bucket holding the next iteration's pairs
+  unsigned long long* cell; // [C][n][2] argmax maxima from K2 (reset here)
+  const float* keys;        // fp32 scan keys (exact tie resolution)
+  uint64_t Sp;
   const uint8_t* props;     // [C][iters+1][2] proposal positions (a,b)
   const double* thr;        // [C][iters+1] log10(u_t) of the acceptance stream
   uint64_t* tmasks;         // [C][K][n] tracker graphs
@@ -42,9 +54,10 @@ struct StepArgs {
   double* tr_prop;          // [C][iters]
   uint8_t* tr_acc;          // [C][iters]
   double* tr_best;          // [C][iters]
-  unsigned long long* stat_rows;  // rows rescanned (sum)
+  unsigned long long* stat_rows;  // rows rescanned (sum over chains and iterations)
+  int* error;               // internal-consistency flag
   uint64_t iters;
-  int n, G, K, strict;
+  int n, K, strict;
   int score_only;           // bnmc_gpu_score_orders: write graphs, no chain logic
   uint64_t* out_masks;      // score_only outputs [C][n]
   double* out_best;         // [C][n]
@@ -52,203 +65,300 @@ struct StepArgs {
   TieCtx tie;
 };
 
-// precedes (sampler.cpp:16-19): total desc, then Dag operator< (lexicographic
-// over the parent masks, types.hpp:140-142).
-__device__ __forceinline__ bool dag_less(const uint64_t* a, const uint64_t* b, int n) {
-  for (int i = 0; i < n; ++i)
-    if (a[i] != b[i]) return a[i] < b[i];
-  return false;
-}
+constexpr int kStepThreads = 256;
+constexpr int kTrackerSmem = 2048;  // u64 slots for staging tracker shifts
 
-// Prepare the rescan items of the proposed order `prop` for positions lo..hi.
-__device__ void prepare_items(const StepArgs& A, int c, const uint8_t* prop, int lo, int hi) {
-  uint64_t pred = 0;
-  Item* items = A.items + (uint64_t)c * A.n;
-  for (int p = 0; p < hi + 1; ++p) {
-    const int v = prop[p];
-    if (p >= lo) {
-      Item it;
-      it.cpred = nodes_to_cand(pred, v);
-      it.v = (uint32_t)v;
-      it.pad = 0;
-      items[p - lo] = it;
-    }
-    pred |= 1ull << v;
+// Rescan pairs of the proposed order `prop` for positions lo..hi into bucket
+// `nb` (and the chain's own item list), plus the position table. Warp 0:
+// prefix-OR of predecessor bits by shuffle.
+__device__ void prepare_items_warp(const StepArgs& A, int c, const uint8_t* prop, int lo, int hi,
+                                   int nb) {
+  const int lane = threadIdx.x & 31;
+  const int n = A.n;
+  uint64_t bit[2], pre[2];
+  bit[0] = 2 * lane < n ? 1ull << prop[2 * lane] : 0ull;
+  bit[1] = 2 * lane + 1 < n ? 1ull << prop[2 * lane + 1] : 0ull;
+  uint64_t incl = bit[0] | bit[1];
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const uint64_t o = __shfl_up_sync(0xffffffffu, incl, off);
+    if (lane >= off) incl |= o;
   }
-  for (int p = 0; p < A.n; ++p) A.ppos[64 * c + prop[p]] = (uint8_t)p;
-  A.counts[c] = hi - lo + 1;
+  pre[0] = incl & ~(bit[0] | bit[1]);
+  pre[1] = pre[0] | bit[0];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int p = 2 * lane + h;
+    if (p >= n) continue;
+    const int v = prop[p];
+    A.ppos[64 * c + v] = (uint8_t)p;
+    if (p < lo || p > hi) continue;
+    const uint64_t cpred = nodes_to_cand(pre[h], v);
+    Item it;
+    it.cpred = cpred;
+    it.v = (uint32_t)v;
+    it.pad = 0;
+    A.items[64 * c + (p - lo)] = it;
+    const int pos = atomicAdd(&A.rowcnt[nb * n + v], 1);
+    PairRec pr;
+    pr.cpred = cpred;
+    pr.chain = (uint16_t)c;
+    pr.slot = (uint16_t)(p - lo);
+    pr.v = (uint32_t)v;
+    A.buckets[(nb * n + v) * kMaxChains + pos] = pr;
+  }
+  if (lane == 0) A.counts[c] = hi - lo + 1;
 }
 
-template <typename K>
-__global__ void __launch_bounds__(256) step_kernel(StepArgs A) {
+// Exact argmax of row v among admissible entries whose fp32 key has order
+// image `okey` (the cells reported a key tie). Whole CTA; rare path.
+__device__ uint32_t resolve_tie(const StepArgs& A, int v, uint64_t cpred, uint32_t okey,
+                                const uint8_t* ppos, uint32_t* s_cand) {
+  uint32_t best = kNoIdx;
+  const float* row = A.keys + (uint64_t)v * A.Sp;
+  for (uint64_t g = threadIdx.x; g < A.tie.S; g += blockDim.x) {
+    if (ordkey(row[g]) != okey) continue;
+    if ((A.tie.cmask[g] & ~cpred) != 0) continue;
+    if (best == kNoIdx || better_slow(A.tie, v, (uint32_t)g, best, ppos)) best = (uint32_t)g;
+  }
+  s_cand[threadIdx.x] = best;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t w = kNoIdx;
+    for (int i = 0; i < (int)blockDim.x; ++i) {
+      const uint32_t g = s_cand[i];
+      if (g != kNoIdx && (w == kNoIdx || better_slow(A.tie, v, g, w, ppos))) w = g;
+    }
+    s_cand[0] = w;
+  }
+  __syncthreads();
+  const uint32_t w = s_cand[0];
+  __syncthreads();
+  return w;
+}
+
+__global__ void __launch_bounds__(kStepThreads) step_kernel(StepArgs A) {
   const int c = blockIdx.x;
-  ChainState* st = A.st + c;
-  __shared__ uint64_t s_newm[64];
-  __shared__ double s_newb[64];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  constexpr int kWarps = kStepThreads / 32;
   __shared__ uint64_t s_pm[64];
   __shared__ double s_pb[64];
-  __shared__ uint8_t s_prop[64];
-  __shared__ uint8_t s_ppos[64];
-  __shared__ int s_v[64];
-  __shared__ double s_total;
-  __shared__ int s_insert, s_dup;
-  if (!A.score_only && st->done) return;
+  __shared__ uint8_t s_order[64], s_prop[64], s_ppos[64];
+  __shared__ Item s_item[64];
+  __shared__ uint32_t s_g[64];
+  __shared__ uint32_t s_key[64];
+  __shared__ int s_tie[64];
+  __shared__ double s_total, s_cur_total;
+  __shared__ int s_cnt, s_done, s_tcount, s_go, s_anytie;
+  __shared__ uint64_t s_iter;
+  __shared__ uint64_t s_stage[kTrackerSmem];
+  __shared__ uint32_t s_cand[kStepThreads];
+  cudaGridDependencySynchronize();
+  ChainState* st = A.st + c;
   const int n = A.n;
-  const int cnt = A.counts[c];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (threadIdx.x < 64) {
-    if (!A.score_only) s_prop[threadIdx.x] = st->prop[threadIdx.x];
-    s_ppos[threadIdx.x] = A.ppos[64 * c + threadIdx.x];
+  if (tid == 0) {
+    s_cnt = A.counts[c];
+    s_anytie = 0;
+    if (A.score_only) {
+      s_done = 0;
+    } else {
+      s_done = st->done;
+      s_iter = st->iter;
+      s_cur_total = st->total;
+      s_tcount = st->tcount;
+    }
+  }
+  if (tid < 64) {
+    s_ppos[tid] = A.ppos[64 * c + tid];
+    s_item[tid] = A.items[64 * c + tid];
+    if (!A.score_only && tid < n) {
+      s_prop[tid] = st->prop[tid];
+      s_pm[tid] = st->masks[tid];
+      s_pb[tid] = st->best[tid];
+      s_order[tid] = st->order[tid];
+    }
   }
   __syncthreads();
-  const Partial<K>* parts = static_cast<const Partial<K>*>(A.partials);
-  // 1. argmax_reduce over the G CTA cells of every rescanned row.
-  for (int s = warp; s < cnt; s += blockDim.x >> 5) {
-    const int v = A.items[(uint64_t)c * n + s].v;
-    K k = (K)-INFINITY;
-    uint32_t g = kNoIdx;
-    for (int b = lane; b < A.G; b += 32) {
-      const Partial<K> p = parts[((uint64_t)c * n + s) * A.G + b];
-      if (better<K>(A.tie, v, p.k, p.g, k, g, s_ppos)) {
-        k = p.k;
-        g = p.g;
+  // Bucket housekeeping for the next scan (CTA 0): the bucket that this
+  // iteration's scan read is cleared; `sel` points at the one filled below.
+  if (!A.score_only && c == 0 && tid < n) {
+    const int nb = s_done ? *A.sel : (int)(s_iter & 1);
+    A.rowcnt[(1 - nb) * n + tid] = 0;
+    if (s_done) A.rowcnt[nb * n + tid] = 0;
+    if (tid == 0) *A.sel = nb;
+  }
+  if (s_done) return;
+  const int cnt = s_cnt;
+  // 1. the argmax cell of every rescanned row; reset the cells.
+  if (tid < cnt) {
+    unsigned long long* cell = A.cell + 2ull * (c * n + tid);
+    const unsigned long long hi = cell[0], lo = cell[1];
+    cell[0] = 0ull;
+    cell[1] = 0ull;
+    const uint32_t g1 = (uint32_t)hi, g2 = ~(uint32_t)lo;
+    s_key[tid] = (uint32_t)(hi >> 32);
+    s_g[tid] = g1;
+    s_tie[tid] = g1 != g2;
+    if (hi == 0ull) atomicExch(A.error, 3);  // every row admits the empty set
+    if (g1 != g2) s_anytie = 1;
+  }
+  __syncthreads();
+  if (s_anytie) {
+    for (int s = 0; s < cnt; ++s)
+      if (s_tie[s]) {
+        const uint32_t g = resolve_tie(A, s_item[s].v, s_item[s].cpred, s_key[s], s_ppos, s_cand);
+        if (tid == 0) s_g[s] = g;
       }
-    }
-    warp_argmax<K>(A.tie, v, k, g, s_ppos);
-    if (lane == 0) {
-      const uint64_t nm = cand_to_nodes(A.tie.cmask[g], v);
-      s_newm[s] = nm;
-      s_newb[s] = A.tie.ls[(uint64_t)v * A.tie.S + g] + ppf_sum(A.tie.w, n, v, nm);
-      s_v[s] = v;
-    }
+    __syncthreads();
+  }
+  if (tid < cnt) {
+    const int v = s_item[tid].v;
+    const uint32_t g = s_g[tid];
+    const uint64_t nm = cand_to_nodes(A.tie.cmask[g], v);
+    s_pm[v] = nm;
+    s_pb[v] = A.tie.ls[(uint64_t)v * A.tie.S + g] + ppf_sum(A.tie.w, n, v, nm);
   }
   __syncthreads();
-  // 2. proposed graph and total (ascending node order, engine.cpp:95-96).
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < n; ++i) {  // score_only: every row is rescanned below
-      s_pm[i] = A.score_only ? 0ull : st->masks[i];
-      s_pb[i] = A.score_only ? 0.0 : st->best[i];
-    }
-    for (int s = 0; s < cnt; ++s) {
-      s_pm[s_v[s]] = s_newm[s];
-      s_pb[s_v[s]] = s_newb[s];
-    }
+  // 2. proposed total, ascending node order (engine.cpp:95-96).
+  if (tid == 0) {
     double t = 0.0;
     for (int i = 0; i < n; ++i) t += s_pb[i];
     s_total = t;
   }
   __syncthreads();
   if (A.score_only) {
-    if (threadIdx.x < n) {
-      if (A.out_masks) A.out_masks[(uint64_t)c * n + threadIdx.x] = s_pm[threadIdx.x];
-      if (A.out_best) A.out_best[(uint64_t)c * n + threadIdx.x] = s_pb[threadIdx.x];
+    if (tid < n) {
+      if (A.out_masks) A.out_masks[(uint64_t)c * n + tid] = s_pm[tid];
+      if (A.out_best) A.out_best[(uint64_t)c * n + tid] = s_pb[tid];
     }
-    if (threadIdx.x == 0 && A.out_total) A.out_total[c] = s_total;
+    if (tid == 0 && A.out_total) A.out_total[c] = s_total;
     return;
   }
-  const uint64_t t = st->iter;
+  const uint64_t t = s_iter;
   const double proposed = s_total;
-  bool accepted;
-  if (t == 0) {
-    accepted = true;  // initial order: becomes the current state
-  } else {
-    // mh_accept (sampler.cpp:54-56): log10(u) < new - old
-    accepted = A.thr[c * (A.iters + 1) + t] < proposed - st->total;
-  }
-  // 3. BestGraphTracker::update (sampler.cpp:32-41), warp 0.
+  // mh_accept (sampler.cpp:54-56): log10(u) < new - old; the initial order is
+  // adopted as the current state without a draw.
+  const bool accepted = t == 0 ? true : (A.thr[c * (A.iters + 1) + t] < proposed - s_cur_total);
+  // 3. BestGraphTracker::update (sampler.cpp:32-41).
   const bool offer = (t == 0) || accepted || !A.strict;
-  if (warp == 0 && offer) {
-    const int K_ = A.K;
-    uint64_t* tm = A.tmasks + (uint64_t)c * K_ * n;
-    double* tt = A.ttotals + (uint64_t)c * K_;
-    const int count = st->tcount;
+  const int K_ = A.K;
+  uint64_t* tm = A.tmasks + (uint64_t)c * K_ * n;
+  double* tt = A.ttotals + (uint64_t)c * K_;
+  if (offer) {
+    const int count = s_tcount;
     const bool full = count == K_;
-    // A full tracker rejects totals <= its minimum whether or not the graph
-    // is a duplicate, so that test may run first.
-    bool go = !(full && proposed <= tt[count - 1]);
-    if (go) {
-      if (lane == 0) s_dup = 0;
-      __syncwarp();
-      for (int e = lane; e < count; e += 32) {
+    // A full tracker rejects totals <= its minimum whether or not the graph is
+    // a duplicate, so that test runs first.
+    if (tid == 0) s_go = !(full && proposed <= tt[count - 1]);
+    __syncthreads();
+    if (s_go) {
+      int dup_local = 0;  // dedupe by full graph equality
+      for (int e = warp; e < count; e += kWarps) {
         bool eq = true;
-        for (int i = 0; i < n && eq; ++i) eq = tm[(uint64_t)e * n + i] == s_pm[i];
-        if (eq) s_dup = 1;
+        for (int i = lane; i < n; i += 32) eq &= tm[(uint64_t)e * n + i] == s_pm[i];
+        dup_local |= __all_sync(0xffffffffu, eq);
       }
-      __syncwarp();
-      go = !s_dup;
-    }
-    if (go) {
-      // lower_bound with `precedes`: first entry that does not precede g.
-      if (lane == 0) {
-        int pos = 0;
-        while (pos < count) {
-          const double et = tt[pos];
-          const bool prec = (et != proposed) ? (et > proposed)
-                                             : dag_less(tm + (uint64_t)pos * n, s_pm, n);
-          if (!prec) break;
-          ++pos;
+      if (!__syncthreads_or(dup_local)) {
+        // lower_bound with precedes (total desc, then Dag operator<): the
+        // entries preceding g form a prefix of the sorted tracker.
+        int ins = 0;
+        for (int e0 = 0; e0 < count; e0 += kStepThreads) {
+          const int e = e0 + tid;
+          bool prec = false;
+          if (e < count) {
+            const double et = tt[e];
+            if (et != proposed) {
+              prec = et > proposed;
+            } else {
+              for (int i = 0; i < n; ++i) {
+                const uint64_t x = tm[(uint64_t)e * n + i], y = s_pm[i];
+                if (x != y) {
+                  prec = x < y;
+                  break;
+                }
+              }
+            }
+          }
+          ins += __syncthreads_count(prec);
         }
-        s_insert = pos;
-      }
-      __syncwarp();
-      const int pos = s_insert;
-      const int last = full ? count - 1 : count;
-      for (int e = last; e > pos; --e) {
-        for (int i = lane; i < n; i += 32) tm[(uint64_t)e * n + i] = tm[(uint64_t)(e - 1) * n + i];
-        if (lane == 0) tt[e] = tt[e - 1];
-        __syncwarp();
-      }
-      for (int i = lane; i < n; i += 32) tm[(uint64_t)pos * n + i] = s_pm[i];
-      if (lane == 0) {
-        tt[pos] = proposed;
-        if (!full) st->tcount = count + 1;
+        const int last = full ? count - 1 : count;
+        const int moving = last - ins;  // entries [ins, last) move down one slot
+        if ((long long)moving * n <= kTrackerSmem) {
+          for (int idx = tid; idx < moving * n; idx += kStepThreads)
+            s_stage[idx] = tm[(uint64_t)ins * n + idx];
+          __syncthreads();
+          for (int idx = tid; idx < moving * n; idx += kStepThreads)
+            tm[(uint64_t)(ins + 1) * n + idx] = s_stage[idx];
+        } else {
+          for (int e = last; e > ins; --e) {
+            for (int i = tid; i < n; i += kStepThreads)
+              tm[(uint64_t)e * n + i] = tm[(uint64_t)(e - 1) * n + i];
+            __syncthreads();
+          }
+        }
+        if (tid == 0)
+          for (int e = last; e > ins; --e) tt[e] = tt[e - 1];
+        __syncthreads();
+        for (int i = tid; i < n; i += kStepThreads) tm[(uint64_t)ins * n + i] = s_pm[i];
+        if (tid == 0) {
+          tt[ins] = proposed;
+          if (!full) s_tcount = count + 1;
+        }
       }
     }
+    __syncthreads();
   }
-  __syncthreads();
   // 4. commit + trace + next proposal.
-  if (threadIdx.x == 0) {
+  if (accepted && tid < n) {
+    st->masks[tid] = s_pm[tid];
+    st->best[tid] = s_pb[tid];
+    st->order[tid] = s_prop[tid];
+    s_order[tid] = s_prop[tid];
+  }
+  if (tid == 0) {
     if (accepted) {
-      for (int i = 0; i < n; ++i) {
-        st->masks[i] = s_pm[i];
-        st->best[i] = s_pb[i];
-        st->order[i] = s_prop[i];
-      }
       st->total = proposed;
       if (t > 0) st->accepted += 1;
     }
+    st->tcount = s_tcount;
     if (t > 0) {
       const uint64_t o = (uint64_t)c * A.iters + (t - 1);
       A.tr_prop[o] = proposed;
       A.tr_acc[o] = accepted ? 1 : 0;
-      A.tr_best[o] = A.ttotals[(uint64_t)c * A.K];
+      A.tr_best[o] = tt[0];
     }
     atomicAdd(A.stat_rows, (unsigned long long)cnt);
-    const uint64_t nt = t + 1;
-    st->iter = nt;
-    if (nt > A.iters) {
+    st->iter = t + 1;
+  }
+  __syncthreads();
+  const uint64_t nt = t + 1;
+  if (nt > A.iters) {
+    if (tid == 0) {
       st->done = 1;
       A.counts[c] = 0;
-    } else {
-      // propose_swap (sampler.cpp:43-52): positions drawn by the setup kernel.
-      const int pa = A.props[2 * (c * (A.iters + 1) + nt)];
-      const int pb = A.props[2 * (c * (A.iters + 1) + nt) + 1];
-      uint8_t* prop = st->prop;
-      for (int i = 0; i < n; ++i) prop[i] = st->order[i];
-      const uint8_t tmp = prop[pa];
-      prop[pa] = prop[pb];
-      prop[pb] = tmp;
-      st->a = pa;
-      st->b = pb;
-      prepare_items(A, c, prop, min(pa, pb), max(pa, pb));
     }
+    return;
   }
+  // propose_swap (sampler.cpp:43-52): positions drawn by the setup kernel.
+  const int pa = A.props[2 * (c * (A.iters + 1) + nt)];
+  const int pb = A.props[2 * (c * (A.iters + 1) + nt) + 1];
+  if (tid < n) {
+    const int src = tid == pa ? pb : (tid == pb ? pa : tid);
+    s_prop[tid] = s_order[src];
+    st->prop[tid] = s_order[src];
+  }
+  if (tid == 0) {
+    st->a = pa;
+    st->b = pb;
+  }
+  __syncthreads();
+  if (warp == 0) prepare_items_warp(A, c, s_prop, min(pa, pb), max(pa, pb), (int)(t & 1));
 }
 
 // Setup (one thread per chain): initial order = shuffle of the split(1)
 // stream (sampler.cpp:83-86), proposal positions of every iteration from the
 // split(2) stream (propose_swap, sampler.cpp:43-52; the proposal stream does
-// not depend on acceptance), initial items = every row of the initial order.
+// not depend on acceptance).
 __global__ void setup_chains_kernel(StepArgs A, const uint64_t* __restrict__ seeds, int C) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= C) return;
@@ -286,16 +396,30 @@ __global__ void setup_chains_kernel(StepArgs A, const uint64_t* __restrict__ see
     pp[2 * t] = (uint8_t)a;
     pp[2 * t + 1] = (uint8_t)b;
   }
-  prepare_items(A, c, order, 0, n - 1);
 }
 
-// Setup for bnmc_gpu_score_orders: items = every row of each given order.
-__global__ void setup_orders_kernel(StepArgs A, const int* __restrict__ perms, int C) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= C) return;
-  uint8_t order[64];
-  for (int i = 0; i < A.n; ++i) order[i] = (uint8_t)perms[(uint64_t)c * A.n + i];
-  prepare_items(A, c, order, 0, A.n - 1);
+// Initial pairs (every row of each order) into bucket 1; sel = 1. One CTA of
+// 64 threads per order. The buckets' counters and the cells must be zero.
+__global__ void setup_items_kernel(StepArgs A, const int* __restrict__ perms, int C) {
+  const int c = blockIdx.x;
+  __shared__ uint8_t s_prop[64];
+  if (threadIdx.x < A.n)
+    s_prop[threadIdx.x] =
+        perms ? (uint8_t)perms[(uint64_t)c * A.n + threadIdx.x] : A.st[c].order[threadIdx.x];
+  __syncthreads();
+  if (threadIdx.x < 32) prepare_items_warp(A, c, s_prop, 0, A.n - 1, 1);
+  if (c == 0 && threadIdx.x == 0) *A.sel = 1;
+}
+
+// Diagnostics: pairs for positions lo..hi of each order (bnmc_gpu_bench_scan).
+__global__ void setup_items_range_kernel(StepArgs A, const int* __restrict__ perms, int C, int lo,
+                                         int hi) {
+  const int c = blockIdx.x;
+  __shared__ uint8_t s_prop[64];
+  if (threadIdx.x < A.n) s_prop[threadIdx.x] = (uint8_t)perms[(uint64_t)c * A.n + threadIdx.x];
+  __syncthreads();
+  if (threadIdx.x < 32) prepare_items_warp(A, c, s_prop, lo, hi, 1);
+  if (c == 0 && threadIdx.x == 0) *A.sel = 1;
 }
 
 }  // namespace bnmc_dev
