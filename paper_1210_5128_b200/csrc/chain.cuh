@@ -25,6 +25,7 @@ struct ChainState {
   int done;
   int tcount;          // tracker entries
   int a, b;            // pending proposal positions (-1 for the initial scoring)
+  uint64_t tied;       // nodes whose current best is an exact fp64 tie
   uint8_t order[64];   // current order: order[pos] = node
   uint8_t prop[64];    // proposed order
   uint64_t masks[64];  // current graph (parent masks by node)
@@ -68,22 +69,39 @@ struct StepArgs {
 constexpr int kStepThreads = 256;
 constexpr int kTrackerSmem = 2048;  // u64 slots for staging tracker shifts
 
-// Rescan pairs of the proposed order `prop` for positions lo..hi into bucket
-// `nb` (and the chain's own item list), plus the position table. Warp 0:
-// prefix-OR of predecessor bits by shuffle.
+// Rescan pairs of the proposed order `prop`: positions lo..hi (their
+// predecessor sets changed) plus positions after hi whose node's best is an
+// exact tie (`tied`): their predecessor SET is unchanged, but the swapped
+// nodes changed positions, and the reference breaks exact ties by the first
+// maximum in predecessor-POSITION order (engine.cpp:52), so the chosen set can
+// change. Written into bucket `nb` and the chain's own item list, plus the
+// position table. Warp 0: prefix-OR of predecessor bits and slot prefix sums
+// by shuffle.
 __device__ void prepare_items_warp(const StepArgs& A, int c, const uint8_t* prop, int lo, int hi,
-                                   int nb) {
+                                   uint64_t tied, int nb) {
   const int lane = threadIdx.x & 31;
   const int n = A.n;
   uint64_t bit[2], pre[2];
-  bit[0] = 2 * lane < n ? 1ull << prop[2 * lane] : 0ull;
-  bit[1] = 2 * lane + 1 < n ? 1ull << prop[2 * lane + 1] : 0ull;
+  bool take[2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int p = 2 * lane + h;
+    bit[h] = p < n ? 1ull << prop[p] : 0ull;
+    take[h] = p < n && ((p >= lo && p <= hi) || (p > hi && (tied & bit[h])));
+  }
   uint64_t incl = bit[0] | bit[1];
+  int cnt = (int)take[0] + (int)take[1];
 #pragma unroll
   for (int off = 1; off < 32; off <<= 1) {
     const uint64_t o = __shfl_up_sync(0xffffffffu, incl, off);
-    if (lane >= off) incl |= o;
+    const int k = __shfl_up_sync(0xffffffffu, cnt, off);
+    if (lane >= off) {
+      incl |= o;
+      cnt += k;
+    }
   }
+  const int total = __shfl_sync(0xffffffffu, cnt, 31);
+  int slot = cnt - (int)take[0] - (int)take[1];
   pre[0] = incl & ~(bit[0] | bit[1]);
   pre[1] = pre[0] | bit[0];
 #pragma unroll
@@ -92,28 +110,30 @@ __device__ void prepare_items_warp(const StepArgs& A, int c, const uint8_t* prop
     if (p >= n) continue;
     const int v = prop[p];
     A.ppos[64 * c + v] = (uint8_t)p;
-    if (p < lo || p > hi) continue;
+    if (!take[h]) continue;
     const uint64_t cpred = nodes_to_cand(pre[h], v);
     Item it;
     it.cpred = cpred;
     it.v = (uint32_t)v;
     it.pad = 0;
-    A.items[64 * c + (p - lo)] = it;
+    A.items[64 * c + slot] = it;
     const int pos = atomicAdd(&A.rowcnt[nb * n + v], 1);
     PairRec pr;
     pr.cpred = cpred;
     pr.chain = (uint16_t)c;
-    pr.slot = (uint16_t)(p - lo);
+    pr.slot = (uint16_t)slot;
     pr.v = (uint32_t)v;
     A.buckets[(nb * n + v) * kMaxChains + pos] = pr;
+    ++slot;
   }
-  if (lane == 0) A.counts[c] = hi - lo + 1;
+  if (lane == 0) A.counts[c] = total;
 }
 
 // Exact argmax of row v among admissible entries whose fp32 key has order
-// image `okey` (the cells reported a key tie). Whole CTA; rare path.
+// image `okey` (the cells reported a key tie); *tied is set when another
+// admissible entry has exactly the winner's fp64 value. Whole CTA; rare path.
 __device__ uint32_t resolve_tie(const StepArgs& A, int v, uint64_t cpred, uint32_t okey,
-                                const uint8_t* ppos, uint32_t* s_cand) {
+                                const uint8_t* ppos, uint32_t* s_cand, int* tied) {
   uint32_t best = kNoIdx;
   const float* row = A.keys + (uint64_t)v * A.Sp;
   for (uint64_t g = threadIdx.x; g < A.tie.S; g += blockDim.x) {
@@ -133,6 +153,15 @@ __device__ uint32_t resolve_tie(const StepArgs& A, int v, uint64_t cpred, uint32
   }
   __syncthreads();
   const uint32_t w = s_cand[0];
+  const double ew = exact_eff(A.tie, v, w);
+  int mine = 0;
+  for (uint64_t g = threadIdx.x; g < A.tie.S; g += blockDim.x) {
+    if (g == w || ordkey(row[g]) != okey) continue;
+    if ((A.tie.cmask[g] & ~cpred) != 0) continue;
+    mine |= exact_eff(A.tie, v, (uint32_t)g) == ew;
+  }
+  const int any = __syncthreads_or(mine);
+  if (threadIdx.x == 0) *tied = any;
   __syncthreads();
   return w;
 }
@@ -149,8 +178,8 @@ __global__ void __launch_bounds__(kStepThreads) step_kernel(StepArgs A) {
   __shared__ uint32_t s_key[64];
   __shared__ int s_tie[64];
   __shared__ double s_total, s_cur_total;
-  __shared__ int s_cnt, s_done, s_tcount, s_go, s_anytie;
-  __shared__ uint64_t s_iter;
+  __shared__ int s_cnt, s_done, s_tcount, s_go, s_anytie, s_tflag;
+  __shared__ uint64_t s_iter, s_tied, s_tied_new;
   __shared__ uint64_t s_stage[kTrackerSmem];
   __shared__ uint32_t s_cand[kStepThreads];
   cudaGridDependencySynchronize();
@@ -166,6 +195,7 @@ __global__ void __launch_bounds__(kStepThreads) step_kernel(StepArgs A) {
       s_iter = st->iter;
       s_cur_total = st->total;
       s_tcount = st->tcount;
+      s_tied = st->tied;
     }
   }
   if (tid < 64) {
@@ -206,10 +236,24 @@ __global__ void __launch_bounds__(kStepThreads) step_kernel(StepArgs A) {
   if (s_anytie) {
     for (int s = 0; s < cnt; ++s)
       if (s_tie[s]) {
-        const uint32_t g = resolve_tie(A, s_item[s].v, s_item[s].cpred, s_key[s], s_ppos, s_cand);
-        if (tid == 0) s_g[s] = g;
+        const uint32_t g =
+            resolve_tie(A, s_item[s].v, s_item[s].cpred, s_key[s], s_ppos, s_cand, &s_tflag);
+        if (tid == 0) {
+          s_g[s] = g;
+          s_tie[s] = s_tflag;  // now: exact fp64 tie at the maximum
+        }
       }
     __syncthreads();
+  }
+  // Exact-tie status of the proposed graph: rescanned rows take their fresh
+  // status (a unique fp32 maximum is a unique fp64 maximum), others keep theirs.
+  if (tid == 0 && !A.score_only) {
+    uint64_t tnew = s_tied;
+    for (int s = 0; s < cnt; ++s) {
+      const uint64_t b = 1ull << s_item[s].v;
+      tnew = s_tie[s] ? (tnew | b) : (tnew & ~b);
+    }
+    s_tied_new = tnew;
   }
   if (tid < cnt) {
     const int v = s_item[tid].v;
@@ -318,6 +362,8 @@ __global__ void __launch_bounds__(kStepThreads) step_kernel(StepArgs A) {
   if (tid == 0) {
     if (accepted) {
       st->total = proposed;
+      st->tied = s_tied_new;
+      s_tied = s_tied_new;
       if (t > 0) st->accepted += 1;
     }
     st->tcount = s_tcount;
@@ -352,7 +398,7 @@ __global__ void __launch_bounds__(kStepThreads) step_kernel(StepArgs A) {
     st->b = pb;
   }
   __syncthreads();
-  if (warp == 0) prepare_items_warp(A, c, s_prop, min(pa, pb), max(pa, pb), (int)(t & 1));
+  if (warp == 0) prepare_items_warp(A, c, s_prop, min(pa, pb), max(pa, pb), s_tied, (int)(t & 1));
 }
 
 // Setup (one thread per chain): initial order = shuffle of the split(1)
@@ -381,6 +427,7 @@ __global__ void setup_chains_kernel(StepArgs A, const uint64_t* __restrict__ see
   st->done = 0;
   st->tcount = 0;
   st->a = st->b = -1;
+  st->tied = 0;
   for (int i = 0; i < 64; ++i) {
     st->order[i] = i < n ? order[i] : 0;
     st->prop[i] = i < n ? order[i] : 0;
@@ -407,7 +454,7 @@ __global__ void setup_items_kernel(StepArgs A, const int* __restrict__ perms, in
     s_prop[threadIdx.x] =
         perms ? (uint8_t)perms[(uint64_t)c * A.n + threadIdx.x] : A.st[c].order[threadIdx.x];
   __syncthreads();
-  if (threadIdx.x < 32) prepare_items_warp(A, c, s_prop, 0, A.n - 1, 1);
+  if (threadIdx.x < 32) prepare_items_warp(A, c, s_prop, 0, A.n - 1, 0ull, 1);
   if (c == 0 && threadIdx.x == 0) *A.sel = 1;
 }
 
@@ -418,7 +465,7 @@ __global__ void setup_items_range_kernel(StepArgs A, const int* __restrict__ per
   __shared__ uint8_t s_prop[64];
   if (threadIdx.x < A.n) s_prop[threadIdx.x] = (uint8_t)perms[(uint64_t)c * A.n + threadIdx.x];
   __syncthreads();
-  if (threadIdx.x < 32) prepare_items_warp(A, c, s_prop, lo, hi, 1);
+  if (threadIdx.x < 32) prepare_items_warp(A, c, s_prop, lo, hi, 0ull, 1);
   if (c == 0 && threadIdx.x == 0) *A.sel = 1;
 }
 

@@ -1,0 +1,91 @@
+"""CPU, world_size 2 over gloo: the multi-GPU host logic (row-sharded table
+all-gather and the end-of-run chain-record gather) on CPU tensors — the same
+functions run on NCCL device buffers in bench.py."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from paper_1210_5128_b200 import dist as D
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, n, S, q):
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        full = torch.arange(n * S, dtype=torch.float64).view(n, S) * 1.5
+        rows = torch.full((n, S), float("nan"), dtype=torch.float64)
+        a, b = D.row_partition(n, world)[rank]
+        rows[a:b] = full[a:b]
+        D.all_gather_rows(rows, n, world, rank)
+        ok_rows = bool(torch.equal(rows, full))
+
+        class R:  # minimal chain result
+            pass
+        recs = []
+        for c, seed in enumerate(D.chain_seeds(1, rank, 3, step=0, world=world)):
+            r = R()
+            r.seed = int(seed)
+            r.accepted = 10 * rank + c
+            r.tracker_totals = np.array([-100.0 - rank * 3 - c])
+            r.final_score = -200.0
+            r.tracker_masks = np.array([[c, rank, 7]], np.uint64)
+            r.final_order = np.array([2, 0, 1])
+            recs.append(D.chain_record(r, 3))
+        allrec = D.gather_chain_records(np.stack(recs))
+        q.put((rank, ok_rows, allrec))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n", [7, 60])
+def test_gloo_world2_row_allgather_and_chain_gather(n):
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, n, 5, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    out.sort(key=lambda x: x[0])
+    for rank, ok_rows, allrec in out:
+        assert ok_rows
+        assert allrec.shape == (6, 4 + 2 * 3)
+        dec = [D.decode_record(r, 3) for r in allrec]
+        assert [d["seed"] for d in dec] == [1, 2, 3, 4, 5, 6]  # global chain ids
+        best = D.best_overall(allrec, 3)
+        assert best["best_total"] == -100.0 and best["seed"] == 1
+        assert list(best["best_masks"]) == [0, 0, 7]
+    np.testing.assert_array_equal(out[0][2], out[1][2])
+
+
+def test_row_partition_covers_rows():
+    for n in range(1, 65):
+        for w in range(1, 9):
+            parts = D.row_partition(n, w)
+            assert parts[0][0] == 0 and parts[-1][1] == n
+            assert all(parts[i][1] == parts[i + 1][0] for i in range(w - 1))
+            sizes = [b - a for a, b in parts]
+            assert max(sizes) - min(sizes) <= 1
+
+
+def test_chain_seeds_are_global_ids():
+    s = [D.chain_seeds(1, r, 4, step=k, world=2) for k in range(2) for r in range(2)]
+    flat = np.concatenate(s)
+    assert list(flat) == list(range(1, 17))

@@ -1,0 +1,212 @@
+"""GPU parity beyond the BASELINE configs: the reference's edge cases and
+randomized instances through the C-ABI, checked against the plain-C oracle and
+(when present) the unmodified reference in oracle/_ref. Integer/index results
+and fp64 scores bit-exact."""
+import itertools
+
+import numpy as np
+import pytest
+
+import paper_1210_5128_b200 as P
+from paper_1210_5128_b200 import _lib
+from oracle import port, ref
+
+pytestmark = pytest.mark.gpu
+needs_ref = pytest.mark.skipif(not ref.available(), reason="oracle/_ref not built")
+
+
+def rand_instance(seed, n, m, cmax=4):
+    rng = np.random.default_rng(seed)
+    cards = rng.integers(2, cmax + 1, n).astype(np.int32)
+    cells = (rng.integers(0, 1 << 30, (m, n)) % cards).astype(np.uint8)
+    return cells, cards
+
+
+@pytest.mark.parametrize("seed,n,m,s", [(1, 5, 50, 2), (2, 9, 300, 4), (3, 13, 1000, 3),
+                                        (4, 8, 33, 5), (5, 16, 257, 4), (6, 6, 0, 3),
+                                        (7, 2, 10, 1), (8, 1, 10, 4), (9, 10, 64, 0)])
+def test_random_tables_bit_exact(seed, n, m, s):
+    cells, cards = rand_instance(seed, n, m)
+    cfg = P.RunConfig(max_parents=s, gamma=0.3, ess=2.0)
+    t = P.ScoreCache.build(P.Dataset(cards, cells), cfg).table()
+    o = port.cache_build(cells, cards, s, 0.3, 2.0)
+    np.testing.assert_array_equal(t.view(np.uint64), o.view(np.uint64))
+
+
+def test_k2_mode_bit_exact():
+    cells, cards = rand_instance(11, 8, 400)
+    cfg = P.RunConfig(max_parents=3, gamma=0.5, alpha_mode=P.AlphaMode.K2)
+    t = P.ScoreCache.build(P.Dataset(cards, cells), cfg).table()
+    o = port.cache_build(cells, cards, 3, 0.5, 1.0, k2=True)
+    np.testing.assert_array_equal(t.view(np.uint64), o.view(np.uint64))
+
+
+@needs_ref
+def test_count_statistics_bit_exact():
+    cells, cards = rand_instance(12, 9, 777)
+    rng = np.random.default_rng(0)
+    nodes, psets = [], []
+    for _ in range(64):
+        v = int(rng.integers(9))
+        ps = int(rng.integers(1 << 9)) & ~(1 << v)
+        while bin(ps).count("1") > 4:
+            ps &= ps - 1
+        nodes.append(v)
+        psets.append(ps)
+    sizes = [int(np.prod([cards[p] for p in range(9) if ps >> p & 1])) * int(cards[v])
+             for v, ps in zip(nodes, psets)]
+    offs = np.concatenate([[0], np.cumsum(sizes)[:-1]]).astype(np.uint64)
+    out = np.zeros(sum(sizes), np.uint32)
+    cfgs = np.zeros(64, np.uint64)
+    _lib.check(_lib.lib().bnmc_gpu_count_statistics(
+        np.ascontiguousarray(cells).ravel(), cards, 777, 9, 64, np.array(nodes, np.int32),
+        np.array(psets, np.uint64), offs, out, cfgs, 0))
+    for e in range(64):
+        r = ref.count_statistics(cells, cards, nodes[e], psets[e])
+        assert cfgs[e] == r.shape[0]
+        np.testing.assert_array_equal(out[offs[e]:offs[e] + sizes[e]], r.ravel())
+
+
+def test_capacity_and_usage_errors():
+    cells, cards = rand_instance(13, 10, 50)
+    d = P.Dataset(cards, cells)
+    with pytest.raises(P.CapacityError):  # estimate_bytes over the cap, before allocating
+        P.ScoreCache.build(d, P.RunConfig(max_parents=4, memory_cap_bytes=16))
+    with pytest.raises(P.UsageError):
+        P.ScoreCache.build(d, P.RunConfig(max_parents=9))
+    big = P.Dataset([256] * 6, np.zeros((4, 6), np.uint8))
+    with pytest.raises(P.CapacityError):  # beyond the dense device counter
+        P.ScoreCache.build(big, P.RunConfig(max_parents=4))
+    cache = P.ScoreCache.build(d, P.RunConfig(max_parents=2))
+    with pytest.raises(P.DataError):
+        P.OrderScorer(cache).score([0, 1, 2, 3, 4, 5, 6, 7, 8, 8])
+    with pytest.raises(P.DataError):
+        P.run_mcmc(P.Dataset(cards, np.zeros((0, 10), np.uint8)), P.RunConfig(), None)
+
+
+@needs_ref
+def test_exhaustive_n4_all_orders():
+    """criterion 1 / test_scoring.cpp:310-338: every one of the 24 orders."""
+    cells, truth = ref.generate(4, 3, 300, [2] * 4, seed=41, edge_prob=0.5, concentration=0.5,
+                                tags=(11, 12, 13))
+    pri = np.full((4, 4), 0.5)
+    pri[1, 0], pri[3, 2] = 0.75, 0.2
+    cfg = P.RunConfig(max_parents=3)
+    cache = P.ScoreCache.build(P.Dataset([2] * 4, cells), cfg)
+    rc = ref.Cache.build(cells, [2] * 4, 3)
+    perms = np.array(list(itertools.permutations(range(4))), np.int32)
+    masks, best, tot = P.OrderScorer(cache, pri).score_many(perms)
+    for i, perm in enumerate(perms):
+        m, t = rc.score_order(perm, pri)
+        np.testing.assert_array_equal(masks[i], m)
+        assert tot[i] == t
+        assert rc.score_graph(masks[i], pri) == pytest.approx(t, rel=1e-13)
+
+
+@needs_ref
+@pytest.mark.parametrize("strict", [False, True])
+def test_chains_vs_reference_with_priors_and_strict(strict):
+    cells, truth = ref.generate(12, 3, 500, [3] * 12, seed=5, tags=(1, 2, 3))
+    pri = ref.synth_priors(12, truth, seed=5)
+    cfg = P.RunConfig(max_parents=3, iterations=800, track_top=4, strict_paper_tracker=strict)
+    cache = P.ScoreCache.build(P.Dataset([3] * 12, cells), cfg, pri)
+    rc = ref.Cache.build(cells, [3] * 12, 3)
+    seeds = [3, 17, 99]
+    many = P.run_chains(cache, pri, seeds, cfg)
+    for c, seed in enumerate(seeds):
+        r = ref.run_mcmc(cells, [3] * 12, 3, 800, seed, priors=pri, track_top=4, strict=strict,
+                         prebuilt=rc)
+        np.testing.assert_array_equal(many[c].trace_proposed, r.trace_proposed)
+        np.testing.assert_array_equal(many[c].trace_accepted, r.trace_accepted)
+        np.testing.assert_array_equal(many[c].trace_best, r.trace_best)
+        np.testing.assert_array_equal(many[c].tracker_masks, r.tracker_masks)
+        np.testing.assert_array_equal(many[c].final_order, r.final_order)
+        assert many[c].accepted == r.accepted and many[c].final_score == r.final_score
+
+
+def test_tie_heavy_chain_matches_oracle():
+    """m tiny + gamma 1: many exact ties on fp32 AND fp64 keys, every scan cell
+    goes through the exact tie resolution."""
+    cells, cards = rand_instance(21, 10, 3, cmax=2)
+    cfg = P.RunConfig(max_parents=3, gamma=1.0, iterations=300)
+    cache = P.ScoreCache.build(P.Dataset(cards, cells), cfg)
+    t = port.cache_build(cells, cards, 3, 1.0, 1.0)
+    np.testing.assert_array_equal(cache.table(), t)
+    r = P.run_chains(cache, None, [1, 2], cfg)
+    for c, seed in enumerate([1, 2]):
+        o = port.run_mcmc(t, 3, 300, seed)
+        np.testing.assert_array_equal(r[c].trace_proposed, o["trace_proposed"])
+        np.testing.assert_array_equal(r[c].tracker_masks, o["tracker_masks"])
+
+
+def test_set_priors_refold():
+    cells, cards = rand_instance(22, 8, 200)
+    cfg = P.RunConfig(max_parents=3)
+    cache = P.ScoreCache.build(P.Dataset(cards, cells), cfg)
+    t = cache.table()
+    rng = np.random.default_rng(2)
+    perms = np.stack([rng.permutation(8) for _ in range(6)]).astype(np.int32)
+    for k in range(3):
+        pri = np.where(rng.random((8, 8)) < 0.3, rng.choice([0.0, 0.25, 0.75, 1.0], (8, 8)), 0.5)
+        masks, best, tot = P.OrderScorer(cache, pri).score_many(perms)
+        for i in range(6):
+            m, b, tt = port.score_order(t, 3, perms[i], pri)
+            np.testing.assert_array_equal(masks[i], m)
+            assert tot[i] == tt
+
+
+def test_sharded_build_rows_plus_exchange_equals_full():
+    """Row-sharded precompute (the multi-GPU path) on one device: build rows
+    [a,b) on each shard, exchange rows, finalize -> identical table & scores."""
+    import ctypes as C
+    import torch
+    from paper_1210_5128_b200 import dist as D
+    data, pri, cfg, _ = P.baseline_instance("cfg2")
+    full = P.ScoreCache.build(data, cfg, pri)
+    shards = []
+    for r, (a, b) in enumerate(D.row_partition(data.n, 3)):
+        out = C.c_void_p()
+        _lib.check(_lib.lib().bnmc_gpu_table_build_rows(
+            data.cells.reshape(-1), data.cards, data.rows(), data.n, C.byref(cfg.score_params()),
+            _lib.ptr(pri), a, b, C.byref(out)))
+        shards.append((a, b, P.ScoreCache(out.value, data.n, cfg.max_parents, cfg)))
+    dst = D.table_rows_tensor(shards[0][2])
+    for a, b, sc in shards[1:]:
+        dst[a:b] = D.table_rows_tensor(sc)[a:b]
+    torch.cuda.synchronize()
+    _lib.check(_lib.lib().bnmc_gpu_table_finalize(shards[0][2].handle))
+    merged = shards[0][2]
+    merged._priors_key = None if pri is None else np.asarray(pri).tobytes()
+    np.testing.assert_array_equal(merged.table().view(np.uint64), full.table().view(np.uint64))
+    perms = np.stack([np.random.default_rng(i).permutation(data.n) for i in range(8)]).astype(np.int32)
+    a1 = P.OrderScorer(merged, pri).score_many(perms)
+    a2 = P.OrderScorer(full, pri).score_many(perms)
+    for x, y in zip(a1, a2):
+        np.testing.assert_array_equal(x, y)
+
+
+def test_bnsc_upload_download_roundtrip(tmp_path, golden):
+    g = golden("cfg2")
+    cfg = P.RunConfig(max_parents=4)
+    path = str(tmp_path / "c.bnsc")
+    P.write_bnsc(path, g["table"], 20, 4, cfg.gamma, cfg.ess, cfg.alpha_mode)
+    cache = P.ScoreCache.load(path, cfg)
+    np.testing.assert_array_equal(cache.table(), g["table"])
+    cache.save(str(tmp_path / "d.bnsc"))
+    assert open(path, "rb").read() == open(str(tmp_path / "d.bnsc"), "rb").read()
+    assert cache.lookup(3, 0b101) == port.cache_build(g["cells"], g["cards"], 4)[3][
+        port.index_of(20, 4, 3, 0b101)]
+
+
+def test_run_chains_many_chains_and_max():
+    data, pri, cfg, _ = P.baseline_instance("cfg1")
+    cache = P.ScoreCache.build(data, cfg, pri)
+    cfg.iterations = 50
+    seeds = list(range(1, 65))
+    rs = P.run_chains(cache, pri, seeds, cfg)
+    t = cache.table()
+    for c in (0, 31, 63):
+        o = port.run_mcmc(t, 3, 50, seeds[c], pri)
+        np.testing.assert_array_equal(rs[c].trace_proposed, o["trace_proposed"])
+    with pytest.raises(P.UsageError):
+        P.run_chains(cache, pri, list(range(65)), cfg)

@@ -119,3 +119,22 @@ def test_multi_chain_equals_single_chains(golden):
         np.testing.assert_array_equal(many[c].trace_proposed, one.trace_proposed)
         np.testing.assert_array_equal(many[c].tracker_masks, one.tracker_masks)
         assert many[c].accepted == one.accepted
+
+
+def test_cfg4_golden(golden, golden_meta):
+    """Headline scale: table SHA-256, 20 fixed orders and a 200-iteration chain
+    identical to the unmodified reference (tests/golden/golden_cfg4.npz)."""
+    meta = golden_meta["cfg4"]
+    g = golden("cfg4")
+    data, pri, cfg = instance("cfg4")
+    assert sha(data.cells) == meta["cells_sha256"]
+    cache = P.ScoreCache.build(data, cfg, pri)
+    assert sha(cache.table()) == meta["table_sha256"]
+    masks, best, tot = P.OrderScorer(cache, pri).score_many(g["orders"])
+    np.testing.assert_array_equal(masks, g["order_masks"])
+    np.testing.assert_array_equal(tot, g["order_totals"])
+    cfg.iterations, cfg.seed = meta["iterations"], meta["seed"]
+    r = P.run_mcmc(data, cfg, pri, prebuilt=cache)
+    np.testing.assert_array_equal(r.trace_proposed, g["trace_proposed"])
+    np.testing.assert_array_equal(r.tracker_masks, g["tracker_masks"])
+    assert r.accepted == meta["accepted"] and r.final_score == meta["final_score"]

@@ -1,0 +1,178 @@
+"""CPU: the product's host side — C-ABI library loads and exports every
+symbol include/*.h declares, the reference-identical generator, BNSC
+persistence, reference-shaped validation/error behaviour. No GPU compute."""
+import hashlib
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+import paper_1210_5128_b200 as P
+from paper_1210_5128_b200 import _lib, api
+from oracle import port, ref
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+needs_ref = pytest.mark.skipif(not ref.available(), reason="oracle/_ref not built")
+
+
+def declared_functions():
+    names = []
+    for h in ("bnmc_gpu.h", "bnmc_synth.h"):
+        src = open(os.path.join(ROOT, "include", h)).read()
+        src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+        names += re.findall(r"\b(bnmc_\w+)\s*\(", src)
+    return sorted(set(names))
+
+
+def test_library_exports_every_declared_symbol():
+    out = subprocess.check_output(["nm", "-D", "--defined-only", _lib.LIB_PATH], text=True)
+    exported = {line.split()[-1] for line in out.splitlines()}
+    decl = declared_functions()
+    assert len(decl) >= 20
+    missing = [d for d in decl if d not in exported]
+    assert not missing, missing
+    # and the ctypes binding covers exactly the declared surface
+    assert sorted(_lib.SIGNATURES) == decl
+    L = _lib.lib()
+    for d in decl:
+        assert getattr(L, d) is not None
+
+
+def test_library_is_sm100a_only():
+    out = subprocess.check_output(["cuobjdump", "--list-elf", _lib.LIB_PATH], text=True)
+    archs = set(re.findall(r"sm_(\d+a?)", out))
+    assert archs == {"100a"}, archs
+
+
+def test_pure_host_entry_points():
+    L = _lib.lib()
+    assert L.bnmc_gpu_version() >= 10000
+    assert L.bnmc_gpu_table_estimate_bytes(20, 4) == 20 * 5036 * 8  # test_scoring.cpp:141
+    assert L.bnmc_gpu_bounded_subset_count(59, 4) == 489406
+    assert L.bnmc_gpu_bounded_subset_count(63, 5) == 7666240
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg3", "cfg4"])
+def test_generator_is_reference_identical(name, golden_meta):
+    data, pri, cfg, truth = P.baseline_instance(name)
+    meta = golden_meta[name]
+    assert hashlib.sha256(data.cells.tobytes()).hexdigest() == meta["cells_sha256"]
+    g = np.load(os.path.join(ROOT, "tests", "golden", f"golden_{name}.npz"))
+    np.testing.assert_array_equal(truth, g["truth"])
+    if "priors" in g:
+        np.testing.assert_array_equal(pri, g["priors"])
+    assert (pri is None) == (not meta["priors"])
+
+
+@needs_ref
+def test_generator_other_tags_vs_reference():
+    cards = np.array([2, 3, 4, 2, 5, 3, 2], np.int32)
+    for seed, conc in [(11, 0.5), (42, 1.0), (9, 2.0)]:
+        a = P.synth_instance(7, 3, 400, cards, seed=seed, edge_prob=0.4, concentration=conc,
+                             tags=(1, 2, 3))
+        b = ref.generate(7, 3, 400, cards, seed=seed, edge_prob=0.4, concentration=conc,
+                         tags=(1, 2, 3))
+        np.testing.assert_array_equal(a[0], b[0])
+        np.testing.assert_array_equal(a[1], b[1])
+
+
+def test_runconfig_validation_matches_reference_messages():  # types.cpp:111-121
+    for kw, msg in [(dict(max_parents=9), "max-parents"), (dict(gamma=0.0), "gamma"),
+                    (dict(ess=0.0), "ess"), (dict(iterations=0), "iterations"),
+                    (dict(workers=0), "workers"), (dict(track_top=0), "track-top"),
+                    (dict(tasks_per_node=-1), "tasks-per-node")]:
+        with pytest.raises(P.UsageError, match=msg):
+            P.RunConfig(**kw).validate()
+    P.RunConfig().validate()
+
+
+def test_dataset_validation():  # types.cpp:8-26
+    with pytest.raises(P.DataError, match="between 1 and 64"):
+        P.Dataset([], [])
+    with pytest.raises(P.DataError, match="out of range"):
+        P.Dataset([1, 2], [0, 0])
+    with pytest.raises(P.DataError, match="multiple"):
+        P.Dataset([2, 2], [0, 0, 0])
+    with pytest.raises(P.DataError, match="state out of range at row 1, column 0"):
+        P.Dataset([2, 2], [0, 0, 2, 0])
+    d = P.Dataset([2, 3], [0, 2, 1, 1])
+    assert d.n == 2 and d.rows() == 2 and d.state(0, 1) == 2
+
+
+def test_prior_and_order_validation():
+    with pytest.raises(P.DataError):
+        P.PriorMatrix(2, [0.5, 1.5, 0.5, 0.5])
+    with pytest.raises(P.DataError):
+        P.PriorMatrix(2, [0.5, 0.5, 0.5])
+    pm = P.PriorMatrix.neutral(3)
+    assert pm.is_neutral()
+    pm.set(1, 0, 0.9)
+    assert not pm.is_neutral()
+    with pytest.raises(P.DataError, match="permutation"):
+        P.Order([0, 0, 1])
+    o = P.Order([2, 0, 1])
+    assert list(o.positions()) == [1, 2, 0]
+
+
+def test_global_index_python_matches_oracle():
+    rng = np.random.default_rng(3)
+    for _ in range(500):
+        c = int(rng.integers(1, 64))
+        s = int(rng.integers(0, 6))
+        k = int(rng.integers(0, min(s, c) + 1))
+        mask = sum(1 << int(x) for x in rng.choice(c, k, replace=False)) if k else 0
+        assert api._global_index(mask, c, s) == port.global_index(mask, c, s)
+
+
+def test_bnsc_roundtrip_and_header(tmp_path, golden):
+    g = golden("cfg1")
+    cfg = P.RunConfig(max_parents=3)
+    path = str(tmp_path / "t.bnsc")
+    P.write_bnsc(path, g["table"], 11, 3, cfg.gamma, cfg.ess, cfg.alpha_mode)
+    n, s, t = P.read_bnsc(path, cfg)
+    assert (n, s) == (11, 3)
+    np.testing.assert_array_equal(t.view(np.uint64), g["table"].view(np.uint64))
+    with pytest.raises(P.DataError, match="different scoring parameters"):
+        P.read_bnsc(path, P.RunConfig(max_parents=3, gamma=0.2))
+    with pytest.raises(P.DataError, match="not a score cache"):
+        open(path, "r+b").write(b"XXXX")
+        P.read_bnsc(path, cfg)
+
+
+@needs_ref
+def test_bnsc_bytes_identical_to_reference_save(tmp_path, golden):
+    """Our writer and ScoreCache::save (scoring.cpp:194-208) emit identical files,
+    and ScoreCache::load accepts ours."""
+    g = golden("cfg1")
+    cache = ref.Cache.build(g["cells"], g["cards"], 3)
+    a, b = str(tmp_path / "ref.bnsc"), str(tmp_path / "ours.bnsc")
+    cache.save(a)
+    P.write_bnsc(b, g["table"], 11, 3, 0.1, 1.0, P.AlphaMode.BDEU)
+    assert open(a, "rb").read() == open(b, "rb").read()
+    back = ref.Cache.load(b, 3)
+    np.testing.assert_array_equal(back.table(), g["table"])
+
+
+def test_no_cpu_fallback_without_device():
+    """Compute entry points fail loudly (status 5) when no sm_100 device exists."""
+    try:
+        import torch
+        if torch.cuda.is_available():
+            pytest.skip("a GPU is visible")
+    except ImportError:
+        pass
+    assert _lib.device_count() == 0
+    data, pri, cfg, _ = P.baseline_instance("cfg1")
+    with pytest.raises(_lib.CudaError):
+        P.ScoreCache.build(data, cfg, pri)
+
+
+def test_oracle_is_not_imported_by_the_product():
+    pkg = os.path.join(ROOT, "paper_1210_5128_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".cpp", ".hpp", ".h")):
+                src = open(os.path.join(dirpath, f)).read()
+                assert "oracle" not in re.sub(r"#.*|//.*", "", src).replace("oracle/_ref", ""), f
