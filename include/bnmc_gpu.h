@@ -17,6 +17,8 @@
  *     (include/bnmc/engine.hpp:77-78; PpfTable scoring.hpp:96-112)
  *   OrderScorer::score(const Order&) (engine.hpp:80,      bnmc_gpu_score_order(s)
  *     src/engine.cpp:60-98); score_order (scoring.cpp:261-289)
+ *   OrderScorer::scan_slice (engine.hpp:83,               bnmc_gpu_scan_slice
+ *     src/engine.cpp:43-58)
  *   run_mcmc(data, cfg, priors, prebuilt)                 bnmc_gpu_run_chains
  *     (include/bnmc/sampler.hpp:63-65, src/sampler.cpp:58-116)
  *
@@ -130,6 +132,14 @@ int bnmc_gpu_score_orders(bnmc_table* t, const int* perms, int count, uint64_t* 
                           double* best_out, double* totals_out);
 int bnmc_gpu_score_order(bnmc_table* t, const int* perm, uint64_t* masks_out,
                          double* best_out, double* total_out);
+
+/* OrderScorer::scan_slice (engine.hpp:83, engine.cpp:43-58): argmax of the
+ * effective score (lookup + PpfTable::sum, with the table's bound priors) over
+ * PST indices [lo, hi) of the subsets of positions 0..position-1 of `perm`
+ * (the node at `position`); ties keep the smallest index. An empty slice
+ * yields score -inf and idx UINT64_MAX (the ArgmaxCell identity). */
+int bnmc_gpu_scan_slice(bnmc_table* t, const int* perm, int position, uint64_t lo, uint64_t hi,
+                        double* score_out, uint64_t* idx_out);
 
 /* run_mcmc parameters (RunConfig fields of the sampler). */
 typedef struct {

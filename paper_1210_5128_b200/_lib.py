@@ -64,6 +64,8 @@ SIGNATURES = {
                                       _vp, _vp, _vp, _vp, _vp, _vp, C.POINTER(C.c_float)]),
     "bnmc_gpu_last_scan_stats": (C.c_int, [_vp, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64),
                                            C.POINTER(C.c_float), C.POINTER(C.c_uint64)]),
+    "bnmc_gpu_scan_slice": (C.c_int, [_vp, _i32p, C.c_int, C.c_uint64, C.c_uint64,
+                                      C.POINTER(C.c_double), C.POINTER(C.c_uint64)]),
     "bnmc_gpu_bench_scan": (C.c_int, [_vp, _i32p, C.c_int, C.c_int, C.c_int, C.c_int,
                                       C.POINTER(C.c_float)]),
     "bnmc_synth_last_error": (C.c_char_p, []),

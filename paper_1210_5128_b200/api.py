@@ -419,6 +419,20 @@ class OrderScorer:
                                                      _lib.ptr(tot)))
         return masks, best, tot
 
+    def scan_slice(self, position, node, lo, hi, order):
+        """OrderScorer::scan_slice (engine.cpp:43-58) on the device -> (score, idx);
+        the identity (-inf, 2**64-1) for an empty slice."""
+        perm = np.ascontiguousarray(order.perm if isinstance(order, Order) else order, np.int32)
+        if perm.size != self.cache.n():
+            raise DataError("order and cache disagree on node count")
+        if not 0 <= position < perm.size or int(perm[position]) != node:
+            raise UsageError("work slice does not match the order")
+        self.cache.bind_priors(self._pr)
+        sc, ix = C.c_double(), C.c_uint64()
+        _lib.check(_lib.lib().bnmc_gpu_scan_slice(self.cache.handle, perm, position, lo, hi,
+                                                   C.byref(sc), C.byref(ix)))
+        return sc.value, ix.value
+
     def score(self, order) -> ScoredGraph:
         perm = order.perm if isinstance(order, Order) else order
         masks, best, tot = self.score_many(np.asarray(perm)[None, :])

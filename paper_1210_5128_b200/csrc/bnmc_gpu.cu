@@ -337,6 +337,58 @@ void fold(bnmc_table* t) {
   cudaEventDestroy(e1);
 }
 
+// OrderScorer::scan_slice (engine.cpp:43-58) on the device: PST index g of
+// the node at `position` is the global-index subset of POSITIONS 0..p-1
+// (subset_at, combinatorics.cpp:78-90) mapped through the order
+// (apply_candidates), looked up in the node's row (index_of) plus
+// PpfTable::sum. The reference keeps the first maximum in ascending g; the
+// (score desc, g asc) reduction below selects the same entry. One CTA.
+constexpr int kSliceThreads = 512;
+__global__ void __launch_bounds__(kSliceThreads)
+    slice_kernel(const double* __restrict__ ls, const double* __restrict__ w, uint64_t S, int n,
+                 int s, const int* __restrict__ perm, int position, uint64_t lo, uint64_t hi,
+                 double* out_score, uint64_t* out_idx) {
+  __shared__ int s_perm[64];
+  __shared__ double s_best[kSliceThreads];
+  __shared__ uint64_t s_idx[kSliceThreads];
+  if (threadIdx.x < n) s_perm[threadIdx.x] = perm[threadIdx.x];
+  __syncthreads();
+  const int node = s_perm[position];
+  double best = -INFINITY;
+  uint64_t bi = ~0ull;
+  for (uint64_t g = lo + threadIdx.x; g < hi; g += kSliceThreads) {
+    int size = 0;
+    const uint64_t pos_mask = unrank_global(g, position, s, &size);
+    uint64_t nodes = 0;
+    for (uint64_t m = pos_mask; m; m &= m - 1) nodes |= 1ull << s_perm[__ffsll((long long)m) - 1];
+    const uint64_t gi = global_index_dev(nodes_to_cand(nodes, node), n - 1, s);
+    const double eff = ls[(uint64_t)node * S + gi] + ppf_sum(w, n, node, nodes);
+    if (eff > best) {  // ascending g within the thread: strict > keeps the first
+      best = eff;
+      bi = g;
+    }
+  }
+  s_best[threadIdx.x] = best;
+  s_idx[threadIdx.x] = bi;
+  __syncthreads();
+  for (int half = kSliceThreads / 2; half > 0; half >>= 1) {
+    if (threadIdx.x < half) {
+      const double b2 = s_best[threadIdx.x + half];
+      const uint64_t i2 = s_idx[threadIdx.x + half];
+      if (i2 != ~0ull && (b2 > s_best[threadIdx.x] ||
+                          (b2 == s_best[threadIdx.x] && i2 < s_idx[threadIdx.x]))) {
+        s_best[threadIdx.x] = b2;
+        s_idx[threadIdx.x] = i2;
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    *out_score = s_best[0];
+    *out_idx = s_idx[0];
+  }
+}
+
 TieCtx tie_ctx(const bnmc_table* t) {
   TieCtx c;
   c.ls = t->ls.p;
@@ -827,6 +879,38 @@ int bnmc_gpu_run_chains(bnmc_table* t, const uint64_t* seeds, int n_chains,
     t->last_scan_ms = scan_samples ? static_cast<float>(scan_ms / scan_samples) : 0.f;
     t->last_scan_samples = scan_samples;
     t->last_G = g.G;
+  });
+}
+
+int bnmc_gpu_scan_slice(bnmc_table* t, const int* perm, int position, uint64_t lo, uint64_t hi,
+                        double* score_out, uint64_t* idx_out) {
+  return guarded([&] {
+    if (!t) raise(BNMC_USAGE, "null table");
+    const int n = t->n;
+    std::vector<bool> seen(n, false);
+    for (int i = 0; i < n; ++i) {
+      const int v = perm[i];
+      if (v < 0 || v >= n || seen[v]) raise(BNMC_DATA, "order is not a permutation of 0..n-1");
+      seen[v] = true;
+    }
+    if (position < 0 || position >= n) raise(BNMC_USAGE, "slice position out of range");
+    const uint64_t total = bounded_count(position, t->s);
+    if (lo > hi || hi > total) raise(BNMC_USAGE, "slice range outside [0, S(position, s))");
+    *score_out = -INFINITY;
+    *idx_out = ~0ull;
+    if (lo == hi) return;
+    CK(cudaSetDevice(t->dev));
+    t->perms.alloc(std::max<size_t>(t->perms.n, static_cast<size_t>(n)));
+    t->out_best.alloc(std::max<size_t>(t->out_best.n, 1));
+    t->out_masks.alloc(std::max<size_t>(t->out_masks.n, 1));
+    CK(cudaMemcpyAsync(t->perms.p, perm, sizeof(int) * n, cudaMemcpyHostToDevice, t->stream));
+    slice_kernel<<<1, kSliceThreads, 0, t->stream>>>(t->ls.p, t->w.p, t->S, n, t->s, t->perms.p,
+                                                     position, lo, hi, t->out_best.p,
+                                                     t->out_masks.p);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(score_out, t->out_best.p, 8, cudaMemcpyDeviceToHost, t->stream));
+    CK(cudaMemcpyAsync(idx_out, t->out_masks.p, 8, cudaMemcpyDeviceToHost, t->stream));
+    CK(cudaStreamSynchronize(t->stream));
   });
 }
 
