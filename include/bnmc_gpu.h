@@ -146,8 +146,12 @@ typedef struct {
   uint64_t iterations; /* >= 1 */
   int track_top;       /* BestGraphTracker capacity, >= 1 */
   int strict;          /* RunConfig::strict_paper_tracker */
-  int scan_mode;       /* 0 = auto; 1 = fp32 keys + exact fp64 resolve; 2 = fp64 */
+  int scan_mode;       /* 0 = auto (= 2); 1 = full-row scan: fp32 keys streamed per
+                          rescanned row + exact fp64 resolve, CUDA-Graph loop, <= 64
+                          chains per call; 2 = sorted-row walk: fused device-resident
+                          chains, one CTA per chain, any number of chains */
   int timing_sample;   /* every k-th scan launch is bracketed by CUDA events (0 = 8) */
+  int team_warps;      /* sorted walk: warps per chain (0 auto, 1, 2, 4, 8) */
 } bnmc_chain_params;
 
 /* Run n_chains independent chains, chain c seeded with seeds[c] exactly as
@@ -169,9 +173,20 @@ int bnmc_gpu_run_chains(bnmc_table* t, const uint64_t* seeds, int n_chains,
  * (after batching chains per row and skipping sectors no pair can admit), the
  * average device time of one scan launch (CUDA events around every
  * timing_sample-th launch inside the loop, ms) and the number of kernel
- * launches of the loop. n_chains <= 64 per call. */
+ * launches of the loop (scan_mode 1; for the walk path sectors = entries
+ * visited and scan_ms = the fused kernel's time). */
 int bnmc_gpu_last_scan_stats(const bnmc_table* t, uint64_t* row_rescans, uint64_t* sectors,
                              float* scan_ms_avg, uint64_t* kernel_launches);
+
+/* Scan algorithm used by bnmc_gpu_score_order(s) on this table (0 auto = 2
+ * sorted walk, 1 full-row scan, 2 sorted walk). Results are identical. */
+int bnmc_gpu_table_set_scan_mode(bnmc_table* t, int mode);
+
+/* Statistics of the last sorted-walk run_chains call: (chain, row) pairs
+ * rescanned, sorted entries walked, PST entries enumerated (small predecessor
+ * counts), and the device time of the last per-row sort build (ms). */
+int bnmc_gpu_last_walk_stats(const bnmc_table* t, uint64_t* pairs, uint64_t* walked,
+                             uint64_t* enumerated, float* sort_ms);
 
 /* Diagnostics: time the order-scan kernel alone on the rows at positions
  * lo..hi of `count` (<= 64) orders, averaged over `reps` launches (ms). */

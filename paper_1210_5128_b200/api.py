@@ -48,7 +48,8 @@ class RunConfig:
     memory_cap_bytes: int = 4 << 30
     debug_recheck: bool = False
     device: int = 0
-    scan_mode: int = 0  # 0 auto, 1 fp32 keys + exact fp64 resolve, 2 fp64 keys
+    scan_mode: int = 0  # 0 auto (= 2), 1 full-row fp32-key scan (<= 64 chains), 2 sorted walk
+    team_warps: int = 0  # sorted walk: warps per chain (0 auto, 1, 2, 4, 8)
 
     def validate(self):
         """RunConfig::validate (types.cpp:111-121)."""
@@ -392,8 +393,10 @@ class EngineConfig:
 class OrderScorer:
     """OrderScorer (engine.hpp:77-98): greedy order score on the device."""
 
-    def __init__(self, cache: ScoreCache, priors=None, cfg: EngineConfig | None = None):
+    def __init__(self, cache: ScoreCache, priors=None, cfg: EngineConfig | None = None,
+                 scan_mode: int = 0):
         cfg = cfg or EngineConfig()
+        self.scan_mode = scan_mode
         pr = _prior_array(priors)
         if pr is not None and pr.shape[0] != cache.n():
             raise DataError("priors and cache disagree on node count")
@@ -411,6 +414,7 @@ class OrderScorer:
         if n != self.cache.n():
             raise DataError("order and cache disagree on node count")
         self.cache.bind_priors(self._pr)
+        _lib.check(_lib.lib().bnmc_gpu_table_set_scan_mode(self.cache.handle, self.scan_mode))
         masks = np.empty((k, n), np.uint64)
         best = np.empty((k, n), np.float64)
         tot = np.empty(k, np.float64)
@@ -485,7 +489,8 @@ def run_chains(cache: ScoreCache, priors, seeds, cfg: RunConfig):
     tm = np.empty(nc * K * n, np.uint64)
     tt = np.empty(nc * K, np.float64)
     ms = C.c_float()
-    params = _lib.ChainParams(it, K, int(cfg.strict_paper_tracker), cfg.scan_mode, 0)
+    params = _lib.ChainParams(it, K, int(cfg.strict_paper_tracker), cfg.scan_mode, 0,
+                              cfg.team_warps)
     t0 = time.perf_counter()
     _lib.check(_lib.lib().bnmc_gpu_run_chains(cache.handle, seeds, nc, C.byref(params),
                                                _lib.ptr(tp), _lib.ptr(ta), _lib.ptr(tb),

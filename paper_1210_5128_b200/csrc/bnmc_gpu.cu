@@ -20,7 +20,10 @@
 #include <vector>
 
 #include "../../include/bnmc_gpu.h"
+#include <cub/device/device_radix_sort.cuh>
+
 #include "chain.cuh"
+#include "walk.cuh"
 #include "common.cuh"
 #include "host_util.hpp"
 #include "precompute.cuh"
@@ -152,6 +155,19 @@ struct bnmc_table {
   DevBuf<float> key32;
   DevBuf<double> w;
   std::vector<double> h_w;
+  // sorted rows for the walk path (K2W): eff desc + candidate masks, built
+  // lazily after the priors are folded; PST of small predecessor counts.
+  DevBuf<double> seff;
+  DevBuf<uint64_t> scm;
+  bool sorted_valid = false;
+  float sort_ms = 0.f;
+  DevBuf<uint64_t> pst;
+  DevBuf<uint32_t> pst_off;
+  int pe = -1;
+  int scan_mode = 0;  // default for score_orders: 0 auto (walk), 1 full-row scan
+  DevBuf<int> d_fo, d_tc;
+  DevBuf<unsigned long long> d_acc;
+  DevBuf<double> d_fs;
   float build_ms = 0.f, fold_ms = 0.f;
   // chain / order-scoring workspace
   DevBuf<ChainState> st;
@@ -173,6 +189,8 @@ struct bnmc_table {
   DevBuf<uint64_t> out_masks;
   DevBuf<double> out_best, out_total;
   uint64_t last_rescans = 0, last_sectors = 0, last_launches = 0, last_scan_samples = 0;
+  uint64_t last_walked = 0, last_enumerated = 0;
+  int last_team = 0;
   float last_scan_ms = 0.f, last_total_ms = 0.f;
   int last_G = 0;
   ~bnmc_table() {
@@ -321,6 +339,7 @@ void set_priors(bnmc_table* t, const double* prior_r) {
 }
 
 void fold(bnmc_table* t) {
+  t->sorted_valid = false;
   cudaEvent_t e0, e1;
   CK(cudaEventCreate(&e0));
   CK(cudaEventCreate(&e1));
@@ -399,12 +418,141 @@ TieCtx tie_ctx(const bnmc_table* t) {
   return c;
 }
 
+// eff = ls + PpfTable::sum in the scan's association (engine.cpp:50-51), fp64,
+// with each entry's candidate mask: the input of the per-row sort.
+__global__ void eff64_kernel(const double* __restrict__ ls, const uint64_t* __restrict__ cmask,
+                             const double* __restrict__ w, double* eff, uint64_t* cm, int n,
+                             uint64_t S) {
+  const int v = blockIdx.y;
+  for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < S;
+       g += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t m = cmask[g];
+    eff[(uint64_t)v * S + g] = ls[(uint64_t)v * S + g] + ppf_sum(w, n, v, cand_to_nodes(m, v));
+    cm[(uint64_t)v * S + g] = m;
+  }
+}
+
+// PST of predecessor count p (enumerate_bounded_position_sets order,
+// combinatorics.hpp:83-101) for every p with S(p,s) <= kEnumMax: the walk
+// path enumerates those rows instead of walking them.
+void build_pst_small(bnmc_table* t) {
+  std::vector<uint64_t> masks;
+  std::vector<uint32_t> off(1, 0);
+  int pe = -1;
+  for (int p = 0; p < t->n; ++p) {
+    const uint64_t cnt = bounded_count(p, t->s);
+    if (cnt > kEnumMax) break;
+    for (uint64_t j = 0; j < cnt; ++j) {
+      uint64_t r = j;
+      int k = std::min(t->s, p);
+      for (; k >= 0; --k) {
+        const uint64_t block = hbinom(p, k);
+        if (r < block) break;
+        r -= block;
+      }
+      uint64_t m = 0;
+      for (int i = 0, x = 0; i < k; ++i, ++x) {
+        for (uint64_t c; r >= (c = hbinom(p - x - 1, k - i - 1)); ++x) r -= c;
+        m |= 1ull << x;
+      }
+      masks.push_back(m);
+    }
+    off.push_back(static_cast<uint32_t>(masks.size()));
+    pe = p;
+  }
+  t->pe = pe;
+  t->pst.alloc(std::max<size_t>(masks.size(), 1));
+  t->pst_off.alloc(off.size());
+  if (!masks.empty())
+    CK(cudaMemcpyAsync(t->pst.p, masks.data(), masks.size() * 8, cudaMemcpyHostToDevice, t->stream));
+  CK(cudaMemcpyAsync(t->pst_off.p, off.data(), off.size() * 4, cudaMemcpyHostToDevice, t->stream));
+  CK(cudaStreamSynchronize(t->stream));  // host vectors die here
+}
+
+// Sorted rows (descending eff, CUB radix sort per row; stable, so equal
+// values keep ascending g). Rebuilt after every fold.
+void ensure_sorted(bnmc_table* t) {
+  if (t->sorted_valid) return;
+  if (t->pe < 0 && t->pst_off.n == 0) build_pst_small(t);
+  const uint64_t N = static_cast<uint64_t>(t->n) * t->S;
+  t->seff.alloc(N);
+  t->scm.alloc(N);
+  DevBuf<double> keys;
+  DevBuf<uint64_t> vals;
+  keys.alloc(N);
+  vals.alloc(N);
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  CK(cudaEventRecord(e0, t->stream));
+  const unsigned bx = static_cast<unsigned>(std::min<uint64_t>((t->S + 255) / 256, 4096));
+  eff64_kernel<<<dim3(bx, t->n), 256, 0, t->stream>>>(t->ls.p, t->cmask.p, t->w.p, keys.p, vals.p,
+                                                        t->n, t->S);
+  CK(cudaGetLastError());
+  size_t temp_bytes = 0;
+  CK(cub::DeviceRadixSort::SortPairsDescending(nullptr, temp_bytes, keys.p, t->seff.p, vals.p,
+                                               t->scm.p, static_cast<int>(t->S), 0, 64, t->stream));
+  DevBuf<uint8_t> temp;
+  temp.alloc(std::max<size_t>(temp_bytes, 1));
+  for (int v = 0; v < t->n; ++v) {
+    const uint64_t o = static_cast<uint64_t>(v) * t->S;
+    CK(cub::DeviceRadixSort::SortPairsDescending(temp.p, temp_bytes, keys.p + o, t->seff.p + o,
+                                                 vals.p + o, t->scm.p + o, static_cast<int>(t->S),
+                                                 0, 64, t->stream));
+  }
+  CK(cudaEventRecord(e1, t->stream));
+  CK(cudaEventSynchronize(e1));
+  CK(cudaEventElapsedTime(&t->sort_ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  t->sorted_valid = true;
+}
+
+// Team size: warps per chain (8 = one chain per CTA, 1 = one chain per warp).
+// 0 = auto: whole-CTA chains while they fill the GPU at 4 CTAs per SM,
+// otherwise one warp per chain.
+void launch_walk(bnmc_table* t, const WalkArgs& A, int C, int team_warps = 0) {
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, t->dev);
+  int tw = team_warps;
+  if (tw == 0) tw = C <= 4 * sms ? 8 : (C <= 8 * sms ? 4 : (C <= 16 * sms ? 2 : 1));
+  const int per = kWalkThreads / (32 * tw);
+  const unsigned grid = static_cast<unsigned>((C + per - 1) / per);
+  switch (tw) {
+    case 8: walk_chain_kernel<8><<<grid, kWalkThreads, 0, t->stream>>>(A); break;
+    case 4: walk_chain_kernel<4><<<grid, kWalkThreads, 0, t->stream>>>(A); break;
+    case 2: walk_chain_kernel<2><<<grid, kWalkThreads, 0, t->stream>>>(A); break;
+    case 1: walk_chain_kernel<1><<<grid, kWalkThreads, 0, t->stream>>>(A); break;
+    default: raise(BNMC_USAGE, "team_warps must be 0, 1, 2, 4 or 8");
+  }
+  CK(cudaGetLastError());
+  t->last_team = tw;
+}
+
+WalkArgs walk_args(bnmc_table* t) {
+  WalkArgs A{};
+  A.seff = t->seff.p;
+  A.scm = t->scm.p;
+  A.ls = t->ls.p;
+  A.w = t->w.p;
+  A.pst = t->pst.p;
+  A.pst_off = t->pst_off.p;
+  A.pe = t->pe;
+  A.S = t->S;
+  A.n = t->n;
+  A.s = t->s;
+  A.stat = t->stat.p;
+  A.error = t->rowcnt.p + 2 * t->n + 1;
+  return A;
+}
+
 // Accept thresholds: log10(next_unit_open()) of the split(3) stream with the
 // host's glibc log10 — exactly mh_accept's left-hand side (sampler.cpp:54-56).
 // The acceptance stream draws once per iteration whatever the outcome, so it
 // is state-independent and can be materialised before the device loop.
 void accept_thresholds(const uint64_t* seeds, int C, uint64_t iters, std::vector<double>& out) {
   out.assign(static_cast<size_t>(C) * (iters + 1), 0.0);
+#pragma omp parallel for schedule(static)
   for (int c = 0; c < C; ++c) {
     Rng acc = Rng{seeds[c]}.split(3);
     double* o = out.data() + static_cast<size_t>(c) * (iters + 1);
@@ -421,7 +569,7 @@ void ensure_workspace(bnmc_table* t, int C, uint64_t iters, int K) {
   t->buckets.alloc(2ull * n * kMaxChains);
   t->rowcnt.alloc(2ull * n + 2);  // + sel + error
   t->cell.alloc(2ull * C * n);
-  t->stat.alloc(2);
+  t->stat.alloc(4);
   if (iters) {
     t->props.alloc(static_cast<size_t>(C) * (iters + 1) * 2);
     t->thr.alloc(static_cast<size_t>(C) * (iters + 1));
@@ -434,7 +582,7 @@ void ensure_workspace(bnmc_table* t, int C, uint64_t iters, int K) {
   // clean buckets, cells, sel, error flag
   CK(cudaMemsetAsync(t->rowcnt.p, 0, sizeof(int) * (2ull * n + 2), t->stream));
   CK(cudaMemsetAsync(t->cell.p, 0, 16ull * C * n, t->stream));
-  CK(cudaMemsetAsync(t->stat.p, 0, 16, t->stream));
+  CK(cudaMemsetAsync(t->stat.p, 0, 32, t->stream));
 }
 
 StepArgs step_args(bnmc_table* t) {
@@ -473,6 +621,122 @@ ScanArgs scan_args(const bnmc_table* t, const ScanGeom& g) {
   sa.sector_loads = t->stat.p + 1;
   if (const char* e = std::getenv("BNMC_DEBUG_SCAN_EXIT")) sa.debug_exit = std::atoi(e);
   return sa;
+}
+
+int read_error(bnmc_table* t);
+
+// OrderScorer::score for `count` orders through the walk kernel (one CTA per
+// order, every row rescanned).
+void score_orders_walk(bnmc_table* t, const int* perms, int count, uint64_t* masks_out,
+                       double* best_out, double* totals_out) {
+  const int n = t->n;
+  ensure_workspace(t, 1, 0, 0);
+  ensure_sorted(t);
+  t->perms.alloc(static_cast<size_t>(count) * n);
+  t->out_masks.alloc(static_cast<size_t>(count) * n);
+  t->out_best.alloc(static_cast<size_t>(count) * n);
+  t->out_total.alloc(count);
+  CK(cudaMemcpyAsync(t->perms.p, perms, sizeof(int) * count * n, cudaMemcpyHostToDevice, t->stream));
+  WalkArgs A = walk_args(t);
+  A.C = count;
+  A.perms = t->perms.p;
+  A.out_masks = t->out_masks.p;
+  A.out_best = t->out_best.p;
+  A.out_total = t->out_total.p;
+  launch_walk(t, A, count);
+  CK(cudaGetLastError());
+  if (masks_out)
+    CK(cudaMemcpyAsync(masks_out, t->out_masks.p, 8ull * count * n, cudaMemcpyDeviceToHost, t->stream));
+  if (best_out)
+    CK(cudaMemcpyAsync(best_out, t->out_best.p, 8ull * count * n, cudaMemcpyDeviceToHost, t->stream));
+  if (totals_out)
+    CK(cudaMemcpyAsync(totals_out, t->out_total.p, 8ull * count, cudaMemcpyDeviceToHost, t->stream));
+  CK(cudaStreamSynchronize(t->stream));
+}
+
+// run_chains through the fused walk kernel: one CTA per chain for all
+// iterations; one launch per call.
+void run_chains_walk(bnmc_table* t, const uint64_t* seeds, int C, const bnmc_chain_params* params,
+                     double* trace_proposed, uint8_t* trace_accepted, double* trace_best,
+                     int* final_order, double* final_score, uint64_t* accepted, int* tracker_count,
+                     uint64_t* tracker_masks, double* tracker_totals, float* device_ms) {
+  const int n = t->n, K = params->track_top;
+  const uint64_t iters = params->iterations;
+  ensure_workspace(t, 1, 0, 0);  // error flag + stats
+  ensure_sorted(t);
+  t->seeds.alloc(C);
+  t->thr.alloc(static_cast<size_t>(C) * (iters + 1));
+  t->tmasks.alloc(static_cast<size_t>(C) * K * n);
+  t->ttotals.alloc(static_cast<size_t>(C) * K);
+  t->tr_prop.alloc(static_cast<size_t>(C) * iters);
+  t->tr_best.alloc(static_cast<size_t>(C) * iters);
+  t->tr_acc.alloc(static_cast<size_t>(C) * iters);
+  t->d_fo.alloc(static_cast<size_t>(C) * n);
+  t->d_tc.alloc(C);
+  t->d_acc.alloc(C);
+  t->d_fs.alloc(C);
+  std::vector<double> thr;
+  accept_thresholds(seeds, C, iters, thr);
+  CK(cudaMemcpyAsync(t->seeds.p, seeds, 8ull * C, cudaMemcpyHostToDevice, t->stream));
+  CK(cudaMemcpyAsync(t->thr.p, thr.data(), thr.size() * 8, cudaMemcpyHostToDevice, t->stream));
+  WalkArgs A = walk_args(t);
+  A.C = C;
+  A.iters = iters;
+  A.K = K;
+  A.strict = params->strict;
+  A.seeds = t->seeds.p;
+  A.thr = t->thr.p;
+  A.tmasks = t->tmasks.p;
+  A.ttotals = t->ttotals.p;
+  A.tcount = t->d_tc.p;
+  A.tr_prop = t->tr_prop.p;
+  A.tr_acc = t->tr_acc.p;
+  A.tr_best = t->tr_best.p;
+  A.final_order = t->d_fo.p;
+  A.final_score = t->d_fs.p;
+  A.accepted = t->d_acc.p;
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  CK(cudaEventRecord(e0, t->stream));
+  launch_walk(t, A, C, params->team_warps);
+  CK(cudaGetLastError());
+  CK(cudaEventRecord(e1, t->stream));
+  if (trace_proposed)
+    CK(cudaMemcpyAsync(trace_proposed, t->tr_prop.p, 8ull * C * iters, cudaMemcpyDeviceToHost, t->stream));
+  if (trace_accepted)
+    CK(cudaMemcpyAsync(trace_accepted, t->tr_acc.p, 1ull * C * iters, cudaMemcpyDeviceToHost, t->stream));
+  if (trace_best)
+    CK(cudaMemcpyAsync(trace_best, t->tr_best.p, 8ull * C * iters, cudaMemcpyDeviceToHost, t->stream));
+  if (tracker_masks)
+    CK(cudaMemcpyAsync(tracker_masks, t->tmasks.p, 8ull * C * K * n, cudaMemcpyDeviceToHost, t->stream));
+  if (tracker_totals)
+    CK(cudaMemcpyAsync(tracker_totals, t->ttotals.p, 8ull * C * K, cudaMemcpyDeviceToHost, t->stream));
+  if (final_order)
+    CK(cudaMemcpyAsync(final_order, t->d_fo.p, sizeof(int) * C * n, cudaMemcpyDeviceToHost, t->stream));
+  if (final_score)
+    CK(cudaMemcpyAsync(final_score, t->d_fs.p, 8ull * C, cudaMemcpyDeviceToHost, t->stream));
+  if (accepted)
+    CK(cudaMemcpyAsync(accepted, t->d_acc.p, 8ull * C, cudaMemcpyDeviceToHost, t->stream));
+  if (tracker_count)
+    CK(cudaMemcpyAsync(tracker_count, t->d_tc.p, sizeof(int) * C, cudaMemcpyDeviceToHost, t->stream));
+  unsigned long long stats[3] = {0, 0, 0};
+  CK(cudaMemcpyAsync(stats, t->stat.p, 24, cudaMemcpyDeviceToHost, t->stream));
+  CK(cudaStreamSynchronize(t->stream));
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (device_ms) *device_ms = ms;
+  t->last_rescans = stats[0];
+  t->last_sectors = stats[1] + stats[2];  // walk path: entries visited (walked + enumerated)
+  t->last_walked = stats[1];
+  t->last_enumerated = stats[2];
+  t->last_launches = 1;
+  t->last_total_ms = ms;
+  t->last_scan_ms = ms;
+  t->last_scan_samples = 1;
+  t->last_G = C;
 }
 
 int read_error(bnmc_table* t) {
@@ -652,6 +916,12 @@ int bnmc_gpu_score_orders(bnmc_table* t, const int* perms, int count, uint64_t* 
       }
     }
     CK(cudaSetDevice(t->dev));
+    if (t->scan_mode != 1) {
+      score_orders_walk(t, perms, count, masks_out, best_out, totals_out);
+      if (const int err = read_error(t))
+        raise(BNMC_ERR, "walk consistency check failed (" + std::to_string(err) + ")");
+      return;
+    }
     const ScanGeom g = scan_geometry(t, kMaxChainsPerLaunch * n);
     t->perms.alloc(static_cast<size_t>(kMaxChainsPerLaunch) * n);
     t->out_masks.alloc(static_cast<size_t>(count) * n);
@@ -736,14 +1006,21 @@ int bnmc_gpu_run_chains(bnmc_table* t, const uint64_t* seeds, int n_chains,
     if (!params) raise(BNMC_USAGE, "null chain params");
     if (params->iterations < 1) raise(BNMC_USAGE, "iterations must be >= 1");
     if (params->track_top < 1) raise(BNMC_USAGE, "tracker capacity must be >= 1");
-    if (n_chains < 1 || n_chains > kMaxChainsPerLaunch)
-      raise(BNMC_USAGE, "n_chains must lie in [1," + std::to_string(kMaxChainsPerLaunch) + "]");
     if (t->n < 2) raise(BNMC_USAGE, "swap proposal needs at least two nodes");
     const int mode = params->scan_mode;
-    if (mode == 2)
-      raise(BNMC_USAGE, "scan_mode 2 (fp64 keys) is not provided: the fp32-key scan is exact");
-    if (mode < 0 || mode > 2) raise(BNMC_USAGE, "scan_mode must be 0 or 1");
+    if (mode < 0 || mode > 2) raise(BNMC_USAGE, "scan_mode must be 0, 1 or 2");
+    if (n_chains < 1 || (mode == 1 && n_chains > kMaxChainsPerLaunch))
+      raise(BNMC_USAGE, "n_chains must lie in [1," + std::to_string(kMaxChainsPerLaunch) +
+                            "] for scan_mode 1");
     CK(cudaSetDevice(t->dev));
+    if (mode != 1) {
+      run_chains_walk(t, seeds, n_chains, params, trace_proposed, trace_accepted, trace_best,
+                      final_order, final_score, accepted, tracker_count, tracker_masks,
+                      tracker_totals, device_ms);
+      if (const int err = read_error(t))
+        raise(BNMC_ERR, "walk consistency check failed (" + std::to_string(err) + ")");
+      return;
+    }
     const int n = t->n, C = n_chains, K = params->track_top;
     const uint64_t iters = params->iterations;
     const ScanGeom g = scan_geometry(t, C * n);
@@ -911,6 +1188,25 @@ int bnmc_gpu_scan_slice(bnmc_table* t, const int* perm, int position, uint64_t l
     CK(cudaMemcpyAsync(score_out, t->out_best.p, 8, cudaMemcpyDeviceToHost, t->stream));
     CK(cudaMemcpyAsync(idx_out, t->out_masks.p, 8, cudaMemcpyDeviceToHost, t->stream));
     CK(cudaStreamSynchronize(t->stream));
+  });
+}
+
+int bnmc_gpu_table_set_scan_mode(bnmc_table* t, int mode) {
+  return guarded([&] {
+    if (!t) raise(BNMC_USAGE, "null table");
+    if (mode < 0 || mode > 2) raise(BNMC_USAGE, "scan_mode must be 0, 1 or 2");
+    t->scan_mode = mode;
+  });
+}
+
+int bnmc_gpu_last_walk_stats(const bnmc_table* t, uint64_t* pairs, uint64_t* walked,
+                             uint64_t* enumerated, float* sort_ms) {
+  return guarded([&] {
+    if (!t) raise(BNMC_USAGE, "null table");
+    if (pairs) *pairs = t->last_rescans;
+    if (walked) *walked = t->last_walked;
+    if (enumerated) *enumerated = t->last_enumerated;
+    if (sort_ms) *sort_ms = t->sort_ms;
   });
 }
 

@@ -166,10 +166,78 @@ __device__ uint32_t resolve_tie(const StepArgs& A, int v, uint64_t cpred, uint32
   return w;
 }
 
+// BestGraphTracker::update (sampler.cpp:32-41) for one chain, whole CTA:
+// dedupe by full graph equality, reject when full and total <= minimum,
+// insert at lower_bound of (total desc, Dag operator< on the masks). tm/tt
+// are the chain's K x n masks and K totals; pm is the offered graph (shared
+// memory); *s_tcount the entry count (shared).
+__device__ void tracker_offer(uint64_t* tm, double* tt, int K_, int n, const uint64_t* pm,
+                              double proposed, int* s_tcount, int* s_go, uint64_t* s_stage,
+                              int stage_cap = kTrackerSmem) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nthr = blockDim.x, nwarps = nthr >> 5;
+  const int count = *s_tcount;
+  const bool full = count == K_;
+  // A full tracker rejects totals <= its minimum whether or not the graph is
+  // a duplicate, so that test runs first.
+  if (tid == 0) *s_go = !(full && proposed <= tt[count - 1]);
+  __syncthreads();
+  if (*s_go) {
+    int dup_local = 0;
+    for (int e = warp; e < count; e += nwarps) {
+      bool eq = true;
+      for (int i = lane; i < n; i += 32) eq &= tm[(uint64_t)e * n + i] == pm[i];
+      dup_local |= __all_sync(0xffffffffu, eq);
+    }
+    if (!__syncthreads_or(dup_local)) {
+      int ins = 0;
+      for (int e0 = 0; e0 < count; e0 += nthr) {
+        const int e = e0 + tid;
+        bool prec = false;
+        if (e < count) {
+          const double et = tt[e];
+          if (et != proposed) {
+            prec = et > proposed;
+          } else {
+            for (int i = 0; i < n; ++i) {
+              const uint64_t x = tm[(uint64_t)e * n + i], y = pm[i];
+              if (x != y) {
+                prec = x < y;
+                break;
+              }
+            }
+          }
+        }
+        ins += __syncthreads_count(prec);
+      }
+      const int last = full ? count - 1 : count;
+      const int moving = last - ins;  // entries [ins, last) move down one slot
+      if ((long long)moving * n <= stage_cap) {
+        for (int idx = tid; idx < moving * n; idx += nthr) s_stage[idx] = tm[(uint64_t)ins * n + idx];
+        __syncthreads();
+        for (int idx = tid; idx < moving * n; idx += nthr) tm[(uint64_t)(ins + 1) * n + idx] = s_stage[idx];
+      } else {
+        for (int e = last; e > ins; --e) {
+          for (int i = tid; i < n; i += nthr) tm[(uint64_t)e * n + i] = tm[(uint64_t)(e - 1) * n + i];
+          __syncthreads();
+        }
+      }
+      if (tid == 0)
+        for (int e = last; e > ins; --e) tt[e] = tt[e - 1];
+      __syncthreads();
+      for (int i = tid; i < n; i += nthr) tm[(uint64_t)ins * n + i] = pm[i];
+      if (tid == 0) {
+        tt[ins] = proposed;
+        if (!full) *s_tcount = count + 1;
+      }
+    }
+  }
+  __syncthreads();
+}
+
 __global__ void __launch_bounds__(kStepThreads) step_kernel(StepArgs A) {
   const int c = blockIdx.x;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  constexpr int kWarps = kStepThreads / 32;
+  const int tid = threadIdx.x, warp = tid >> 5;
   __shared__ uint64_t s_pm[64];
   __shared__ double s_pb[64];
   __shared__ uint8_t s_order[64], s_prop[64], s_ppos[64];
@@ -285,73 +353,10 @@ __global__ void __launch_bounds__(kStepThreads) step_kernel(StepArgs A) {
   const bool accepted = t == 0 ? true : (A.thr[c * (A.iters + 1) + t] < proposed - s_cur_total);
   // 3. BestGraphTracker::update (sampler.cpp:32-41).
   const bool offer = (t == 0) || accepted || !A.strict;
-  const int K_ = A.K;
-  uint64_t* tm = A.tmasks + (uint64_t)c * K_ * n;
-  double* tt = A.ttotals + (uint64_t)c * K_;
-  if (offer) {
-    const int count = s_tcount;
-    const bool full = count == K_;
-    // A full tracker rejects totals <= its minimum whether or not the graph is
-    // a duplicate, so that test runs first.
-    if (tid == 0) s_go = !(full && proposed <= tt[count - 1]);
-    __syncthreads();
-    if (s_go) {
-      int dup_local = 0;  // dedupe by full graph equality
-      for (int e = warp; e < count; e += kWarps) {
-        bool eq = true;
-        for (int i = lane; i < n; i += 32) eq &= tm[(uint64_t)e * n + i] == s_pm[i];
-        dup_local |= __all_sync(0xffffffffu, eq);
-      }
-      if (!__syncthreads_or(dup_local)) {
-        // lower_bound with precedes (total desc, then Dag operator<): the
-        // entries preceding g form a prefix of the sorted tracker.
-        int ins = 0;
-        for (int e0 = 0; e0 < count; e0 += kStepThreads) {
-          const int e = e0 + tid;
-          bool prec = false;
-          if (e < count) {
-            const double et = tt[e];
-            if (et != proposed) {
-              prec = et > proposed;
-            } else {
-              for (int i = 0; i < n; ++i) {
-                const uint64_t x = tm[(uint64_t)e * n + i], y = s_pm[i];
-                if (x != y) {
-                  prec = x < y;
-                  break;
-                }
-              }
-            }
-          }
-          ins += __syncthreads_count(prec);
-        }
-        const int last = full ? count - 1 : count;
-        const int moving = last - ins;  // entries [ins, last) move down one slot
-        if ((long long)moving * n <= kTrackerSmem) {
-          for (int idx = tid; idx < moving * n; idx += kStepThreads)
-            s_stage[idx] = tm[(uint64_t)ins * n + idx];
-          __syncthreads();
-          for (int idx = tid; idx < moving * n; idx += kStepThreads)
-            tm[(uint64_t)(ins + 1) * n + idx] = s_stage[idx];
-        } else {
-          for (int e = last; e > ins; --e) {
-            for (int i = tid; i < n; i += kStepThreads)
-              tm[(uint64_t)e * n + i] = tm[(uint64_t)(e - 1) * n + i];
-            __syncthreads();
-          }
-        }
-        if (tid == 0)
-          for (int e = last; e > ins; --e) tt[e] = tt[e - 1];
-        __syncthreads();
-        for (int i = tid; i < n; i += kStepThreads) tm[(uint64_t)ins * n + i] = s_pm[i];
-        if (tid == 0) {
-          tt[ins] = proposed;
-          if (!full) s_tcount = count + 1;
-        }
-      }
-    }
-    __syncthreads();
-  }
+  double* tt = A.ttotals + (uint64_t)c * A.K;
+  if (offer)
+    tracker_offer(A.tmasks + (uint64_t)c * A.K * n, A.ttotals + (uint64_t)c * A.K, A.K, n, s_pm,
+                  proposed, &s_tcount, &s_go, s_stage);
   // 4. commit + trace + next proposal.
   if (accepted && tid < n) {
     st->masks[tid] = s_pm[tid];

@@ -1,0 +1,557 @@
+// K2W — sorted-row walk + fused device-resident chains (sm_100a).
+//
+// Exact replacement of OrderScorer::score (engine.cpp:60-98) for every
+// (chain, rescanned row) pair, without streaming whole rows:
+//
+//   * Row v of the table is kept a second time SORTED by the effective score
+//     eff = lookup + PpfTable::sum (engine.cpp:50-51, computed in fp64 in the
+//     scan's association), descending, with each entry's candidate-position
+//     mask. The argmax over the sets admissible for a predecessor set P is the
+//     FIRST admissible entry of the sorted row (mask test cm & ~P == 0). All
+//     admissible entries with exactly that fp64 value follow contiguously (up
+//     to interleaved inadmissible ones); among them the reference keeps the
+//     first maximum in predecessor-POSITION order (engine.cpp:52; SURVEY
+//     §8.1.2), so ties are resolved on positions.
+//   * A node at a small position p has few admissible sets (S(p,s)) while the
+//     first admissible sorted entry can lie deep in its row (its strong
+//     neighbours come later in the order). For S(p,s) <= kEnumMax the warp
+//     instead ENUMERATES the admissible sets in the reference's own PST order
+//     (combinatorics.hpp:83-101): position subset -> node mask -> cache index
+//     (index_of / global_index) -> exact eff; strict '>' per lane and a
+//     (value desc, index asc) reduction reproduce scan_slice + argmax_reduce
+//     exactly.
+//   * One CTA runs one chain for all its iterations (run_mcmc loop body,
+//     sampler.cpp:92-111): propose_swap from the split(2) stream, rescan of the
+//     rows whose predecessor sets changed (positions min(a,b)..max(a,b), plus
+//     rows whose best is an exact tie), total in ascending node order,
+//     mh_accept against the host's glibc log10(u_t), BestGraphTracker::update,
+//     trace row. No per-iteration launch, no host round trip.
+#pragma once
+
+#include "chain.cuh"
+
+namespace bnmc_dev {
+
+constexpr int kWalkThreads = 256;
+constexpr int kWalkWarps = kWalkThreads / 32;
+constexpr int kWalkUnroll = 8;             // entries per lane per walk round
+constexpr int kEnumUnroll = 4;             // independent gathers per lane per enumeration step
+constexpr uint64_t kEnumMax = 1024;        // enumerate when S(p,s) <= this
+
+struct WalkArgs {
+  const double* __restrict__ seff;    // [n][S] eff, sorted descending per row
+  const uint64_t* __restrict__ scm;   // [n][S] candidate masks in the same order
+  const double* __restrict__ ls;      // [n][S] local scores, BNSC order
+  const double* __restrict__ w;       // [n][n] PPF weights
+  const uint64_t* __restrict__ pst;   // position masks of PST(p) for p <= pe, concatenated
+  const uint32_t* __restrict__ pst_off;  // [pe+2]
+  int pe;                              // largest enumerated predecessor count
+  uint64_t S;
+  int n, s;
+  // chains
+  int C;
+  uint64_t iters;
+  int K, strict;
+  const uint64_t* __restrict__ seeds;  // [C]
+  const double* __restrict__ thr;      // [C][iters+1] log10(u_t)
+  uint64_t* tmasks;                    // [C][K][n]
+  double* ttotals;                     // [C][K]
+  int* tcount;                         // [C]
+  double* tr_prop;                     // [C][iters]
+  uint8_t* tr_acc;
+  double* tr_best;
+  int* final_order;                    // [C][n]
+  double* final_score;                 // [C]
+  unsigned long long* accepted;        // [C]
+  unsigned long long* stat;            // [0] pairs [1] walked entries [2] enumerated entries
+  int* error;
+  // score-only (OrderScorer::score for C orders)
+  const int* perms;                    // [C][n] or null
+  uint64_t* out_masks;                 // [C][n]
+  double* out_best;                    // [C][n]
+  double* out_total;                   // [C]
+};
+
+// a precedes b in the reference enumeration over predecessor positions (sizes
+// descending, then lexicographic on sorted positions). Masks are candidate
+// positions of row v; ppos[node] = position in the current order.
+__device__ __forceinline__ bool prefer_pos(uint64_t ma, uint64_t mb, int v, const uint8_t* ppos) {
+  const int sa = __popcll(ma), sb = __popcll(mb);
+  if (sa != sb) return sa > sb;
+  uint64_t pa = 0, pb = 0;
+  for (uint64_t m = ma; m; m &= m - 1) pa |= 1ull << ppos[cand_node(__ffsll((long long)m) - 1, v)];
+  for (uint64_t m = mb; m; m &= m - 1) pb |= 1ull << ppos[cand_node(__ffsll((long long)m) - 1, v)];
+  const uint64_t d = pa ^ pb;
+  return d != 0 && (pa & (d & (0 - d))) != 0;
+}
+
+// global_index (combinatorics.cpp:61-76) with a shared-memory binomial table
+// bt[c * 9 + j] = C(c, j), j <= 8.
+__device__ __forceinline__ uint64_t gidx_smem(uint64_t mask, int c, int s, const uint64_t* bt) {
+  const int k = __popcll(mask);
+  uint64_t idx = 0;
+  for (int j = k + 1; j <= s; ++j) idx += bt[c * 9 + j];
+  int prev = 0, i = 0;
+  for (uint64_t m = mask; m; m &= m - 1, ++i) {
+    const int a = __ffsll((long long)m);
+    idx += bt[(c - prev) * 9 + (k - i)] - bt[(c - a + 1) * 9 + (k - i)];
+    prev = a;
+  }
+  return idx;
+}
+
+// subset_at (combinatorics.cpp:78-90): the position subset at PST index j of
+// c positions (sizes s..0, lexicographic within a size), smem binomials.
+__device__ __forceinline__ uint64_t unrank_bt(uint32_t j, int c, int s, const uint64_t* bt) {
+  int k = s < c ? s : c;
+  uint64_t r = j;
+  for (; k > 0; --k) {
+    const uint64_t block = bt[c * 9 + k];
+    if (r < block) break;
+    r -= block;
+  }
+  uint64_t mask = 0;
+  int x = 0;
+  for (int i = 0; i < k; ++i, ++x) {
+    for (uint64_t cnt; r >= (cnt = bt[(c - x - 1) * 9 + (k - i - 1)]); ++x) r -= cnt;
+    mask |= 1ull << x;
+  }
+  return mask;
+}
+
+__device__ __forceinline__ double shfl_d(double x, int src) {
+  return __hiloint2double(__shfl_sync(0xffffffffu, __double2hiint(x), src),
+                          __shfl_sync(0xffffffffu, __double2loint(x), src));
+}
+__device__ __forceinline__ uint64_t shfl_u64(uint64_t x, int src) {
+  return ((uint64_t)__shfl_sync(0xffffffffu, (unsigned)(x >> 32), src) << 32) |
+         __shfl_sync(0xffffffffu, (unsigned)x, src);
+}
+
+struct WalkHit {
+  uint64_t start = ~0ull;  // sorted index of the first admissible entry
+  double kstar = 0.0;      // its eff
+  uint64_t kcm = 0;        // its candidate mask
+  bool next_differs = false;  // the next sorted entry is known to hold another value
+};
+
+// One walk round of U entries per lane at sorted indices [base, base + 32U);
+// advances base; true once the first admissible entry is found.
+template <int U>
+__device__ __forceinline__ bool walk_round(const double* re, const uint64_t* rc, uint64_t ncp,
+                                           uint64_t S, uint64_t& base, int lane, WalkHit& h) {
+  if (base >= S) return false;
+  double e[U];
+  uint64_t c[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const uint64_t i = base + u * 32 + lane;
+    e[u] = i < S ? __ldg(re + i) : -INFINITY;
+    c[u] = i < S ? __ldg(rc + i) : ~0ull;
+  }
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const unsigned bal = __ballot_sync(0xffffffffu, (c[u] & ncp) == 0);
+    if (bal && h.start == ~0ull) {
+      const int f = __ffs(bal) - 1;
+      h.start = base + u * 32 + f;
+      h.kstar = shfl_d(e[u], f);
+      h.kcm = shfl_u64(c[u], f);
+      // value of the next sorted entry, when it is in this round's registers
+      const bool known = f < 31 || u + 1 < U;
+      const double nx = f < 31 ? shfl_d(e[u], f + 1) : shfl_d(e[u + 1 < U ? u + 1 : u], 0);
+      h.next_differs = known && nx != h.kstar;
+    }
+  }
+  base += 32 * U;
+  return h.start != ~0ull;
+}
+
+struct PairOut {
+  double eff;
+  uint64_t cm;  // candidate mask of the chosen set
+  int tied;     // another admissible set has exactly the same eff
+};
+
+// Warp-cooperative exact argmax of row v for the node at position p whose
+// predecessors are `cpred` (candidate positions). order[pos] = node, ppos[node]
+// = pos of the order being scored; bt = binomial table in shared memory.
+__device__ PairOut pair_argmax(const WalkArgs& A, int v, int p, uint64_t cpred, const uint8_t* order,
+                               const uint8_t* ppos, const uint64_t* bt, unsigned long long* walked,
+                               unsigned long long* enumerated) {
+  const int lane = threadIdx.x & 31;
+  PairOut r;
+  if (p <= A.pe) {
+    // ---- enumeration in PST order (exact fp64, first maximum wins). Lane l
+    // takes PST indices l, l+32, ...: ascending per lane, so strict '>' keeps
+    // the first maximum; kEnumUnroll independent gathers are in flight.
+    uint32_t cnt = 0;
+    for (int j = 0; j <= A.s && j <= p; ++j) cnt += (uint32_t)bt[p * 9 + j];
+    double best = -INFINITY;
+    uint32_t bj = 0xFFFFFFFFu;
+    bool dup = false;
+    for (uint32_t j0 = 0; j0 < cnt; j0 += 32 * kEnumUnroll) {
+      uint64_t nm[kEnumUnroll];
+      double lv[kEnumUnroll];
+#pragma unroll
+      for (int u = 0; u < kEnumUnroll; ++u) {
+        const uint32_t j = j0 + u * 32 + lane;
+        nm[u] = 0;
+        lv[u] = -INFINITY;
+        if (j < cnt) {
+          const uint64_t pm = unrank_bt(j, p, A.s, bt);
+          for (uint64_t m = pm; m; m &= m - 1) nm[u] |= 1ull << order[__ffsll((long long)m) - 1];
+          const uint64_t g = gidx_smem(nodes_to_cand(nm[u], v), A.n - 1, A.s, bt);
+          lv[u] = __ldg(A.ls + (uint64_t)v * A.S + g);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kEnumUnroll; ++u) {
+        const uint32_t j = j0 + u * 32 + lane;
+        if (j >= cnt) continue;
+        const double e = lv[u] + ppf_sum(A.w, A.n, v, nm[u]);
+        if (e > best) {
+          best = e;
+          bj = j;
+          dup = false;
+        } else if (e == best) {
+          dup = true;
+        }
+      }
+    }
+    double m = best;
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    const bool at_max = best == m && bj != 0xFFFFFFFFu;
+    const unsigned win = __ballot_sync(0xffffffffu, at_max);
+    const uint32_t jmin = __reduce_min_sync(0xffffffffu, at_max ? bj : 0xFFFFFFFFu);
+    r.tied = __popc(win) > 1 || __any_sync(0xffffffffu, at_max && dup);
+    r.eff = m;
+    const uint64_t pm = unrank_bt(jmin, p, A.s, bt);
+    uint64_t nm = 0;
+    for (uint64_t q = pm; q; q &= q - 1) nm |= 1ull << order[__ffsll((long long)q) - 1];
+    r.cm = nodes_to_cand(nm, v);
+    if (lane == 0) *enumerated += cnt;
+    return r;
+  }
+  // ---- walk of the sorted row
+  const double* re = A.seff + (uint64_t)v * A.S;
+  const uint64_t* rc = A.scm + (uint64_t)v * A.S;
+  const uint64_t ncp = ~cpred;
+  const uint64_t S = A.S;
+  WalkHit h;
+  // Rounds grow 32, 64, 128, then 256 entries: most first admissible entries
+  // sit in the first 32, deep walks still get 8 loads per lane in flight.
+  uint64_t base = 0;
+  if (walk_round<1>(re, rc, ncp, S, base, lane, h) || walk_round<2>(re, rc, ncp, S, base, lane, h) ||
+      walk_round<4>(re, rc, ncp, S, base, lane, h)) {
+  } else {
+    while (base < S && !walk_round<kWalkUnroll>(re, rc, ncp, S, base, lane, h)) {
+    }
+  }
+  const uint64_t start = h.start;
+  const bool next_differs = h.next_differs;
+  const double kstar = h.kstar;
+  const uint64_t kcm = h.kcm;
+  if (start == ~0ull) {  // cannot happen: the empty set is admissible in every row
+    if (lane == 0) atomicExch(A.error, 4);
+    r.eff = -INFINITY;
+    r.cm = 0;
+    r.tied = 0;
+    return r;
+  }
+  if (lane == 0) *walked += base;
+  r.eff = kstar;
+  r.cm = kcm;
+  r.tied = 0;
+  // Fast exit: the entry after `start` is still in registers of this round and
+  // has a different value (exact ties are rare), so no tie is possible.
+  if (next_differs) return r;
+  // Tie collection: admissible entries after `start` with eff == kstar.
+  uint64_t best_cm = kcm;
+  int ties = 0;
+  for (uint64_t i0 = start + 1;; i0 += 32) {
+    const uint64_t i = i0 + lane;
+    const bool eq = i < S && __ldg(re + i) == kstar;
+    const uint64_t cm = eq ? __ldg(rc + i) : ~0ull;
+    const bool adm = eq && (cm & ncp) == 0;
+    const unsigned bal = __ballot_sync(0xffffffffu, adm);
+    if (bal) {
+      ties += __popc(bal);
+      // lane-local candidate, then a shuffle reduction under prefer_pos
+      uint64_t mine = adm ? cm : ~0ull;
+      for (int o = 16; o > 0; o >>= 1) {
+        const uint64_t other = shfl_u64(mine, lane ^ o);
+        if (other != ~0ull && (mine == ~0ull || prefer_pos(other, mine, v, ppos))) mine = other;
+      }
+      if (prefer_pos(mine, best_cm, v, ppos)) best_cm = mine;
+    }
+    if (__ballot_sync(0xffffffffu, eq) != 0xffffffffu) break;
+  }
+  r.cm = best_cm;
+  r.tied = ties > 0;
+  return r;
+}
+
+// BestGraphTracker::update (sampler.cpp:32-41) by one warp: dedupe by full
+// graph equality, reject when full and total <= the minimum, insert at the
+// lower bound of (total desc, Dag operator< over the parent masks).
+__device__ void tracker_offer_warp(uint64_t* tm, double* tt, int K, int n, const uint64_t* pm,
+                                   double proposed, int* tcount) {
+  const int lane = threadIdx.x & 31;
+  const int count = *tcount;
+  const bool full = count == K;
+  if (full && proposed <= tt[count - 1]) return;
+  for (int e = 0; e < count; ++e) {
+    bool eq = true;
+    for (int i = lane; i < n; i += 32) eq &= tm[(uint64_t)e * n + i] == pm[i];
+    if (__all_sync(0xffffffffu, eq)) return;
+  }
+  int ins = 0;
+  for (int e0 = 0; e0 < count; e0 += 32) {
+    const int e = e0 + lane;
+    bool prec = false;
+    if (e < count) {
+      const double et = tt[e];
+      if (et != proposed) {
+        prec = et > proposed;
+      } else {
+        for (int i = 0; i < n; ++i) {
+          const uint64_t x = tm[(uint64_t)e * n + i], y = pm[i];
+          if (x != y) {
+            prec = x < y;
+            break;
+          }
+        }
+      }
+    }
+    ins += __popc(__ballot_sync(0xffffffffu, prec));
+  }
+  const int last = full ? count - 1 : count;
+  for (int e = last; e > ins; --e) {  // move entries [ins, last) down one slot
+    for (int i = lane; i < n; i += 32) tm[(uint64_t)e * n + i] = tm[(uint64_t)(e - 1) * n + i];
+    if (lane == 0) tt[e] = tt[e - 1];
+    __syncwarp();
+  }
+  for (int i = lane; i < n; i += 32) tm[(uint64_t)ins * n + i] = pm[i];
+  if (lane == 0) {
+    tt[ins] = proposed;
+    if (!full) *tcount = count + 1;
+  }
+  __syncwarp();
+}
+
+// Barrier over the TW warps of one team (a team runs one chain).
+template <int TW>
+__device__ __forceinline__ void team_sync(int team) {
+  if constexpr (TW == 1) {
+    __syncwarp();
+  } else if constexpr (TW * 32 == kWalkThreads) {
+    __syncthreads();
+  } else {
+    asm volatile("bar.sync %0, %1;" ::"r"(team + 1), "r"(TW * 32) : "memory");
+  }
+}
+
+// Per-team chain state in shared memory.
+struct TeamState {
+  uint8_t order[64], prop[64], ppos[64];
+  uint8_t pv[64], pp[64], pt[64];  // pair -> node, position, exact-tie flag
+  uint64_t pc[64];                 // pair -> candidate predecessor mask
+  uint64_t pm[64];                 // proposed graph (parent node masks by node)
+  double pb[64];                   // proposed per-node bests
+  uint64_t cm[64];                 // current graph
+  double cb[64];                   // current per-node bests
+  uint64_t tied, tied_new, rng;
+  double total, cur_total;
+  unsigned long long acc;
+  int np, a, b, accept, tcount;
+};
+
+// TW warps per chain, kWalkThreads / (32 TW) chains per CTA. TW = 8 gives one
+// chain the whole CTA (lowest latency per iteration); TW = 1 runs a chain per
+// warp, barrier-free, for throughput over many chains.
+template <int TW>
+__global__ void __launch_bounds__(kWalkThreads, 4) walk_chain_kernel(WalkArgs A) {
+  constexpr int kTeams = kWalkThreads / (32 * TW);
+  __shared__ uint64_t s_bt[65 * 9];
+  __shared__ TeamState s_team[kTeams];
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int team = (tid >> 5) / TW, twarp = (tid >> 5) % TW, ttid = tid - team * TW * 32;
+  const int c = blockIdx.x * kTeams + team;
+  const int n = A.n;
+  for (int i = tid; i < 65 * 9; i += kWalkThreads) s_bt[i] = binom(i / 9, i % 9);
+  __syncthreads();
+  if (c >= A.C) return;  // whole teams only: no later CTA-wide barrier when TW < 8
+  TeamState& S = s_team[team];
+  const bool score_only = A.perms != nullptr;
+  uint64_t* tm = score_only ? nullptr : A.tmasks + (uint64_t)c * A.K * n;
+  double* tt = score_only ? nullptr : A.ttotals + (uint64_t)c * A.K;
+  if (ttid == 0) {
+    if (score_only) {
+      for (int i = 0; i < n; ++i) S.order[i] = (uint8_t)A.perms[(uint64_t)c * n + i];
+    } else {
+      // initial order: shuffle of the split(1) stream (sampler.cpp:83-86)
+      const Rng master{A.seeds[c]};
+      Rng init = master.split(1);
+      for (int i = 0; i < n; ++i) S.order[i] = (uint8_t)i;
+      for (int i = n; i > 1; --i) {
+        const int j = (int)init.next_below((uint64_t)i);
+        const uint8_t t = S.order[i - 1];
+        S.order[i - 1] = S.order[j];
+        S.order[j] = t;
+      }
+      S.rng = master.split(2).s;
+    }
+    S.tied = 0;
+    S.tcount = 0;
+    S.acc = 0;
+    S.cur_total = 0.0;
+  }
+  team_sync<TW>(team);
+  unsigned long long walked = 0, enumerated = 0, pairs = 0;
+  double thr_t = 0.0;
+  const uint64_t T = score_only ? 0 : A.iters;
+  for (uint64_t t = 0; t <= T; ++t) {
+    // ---- proposal: propose_swap (sampler.cpp:43-52) from the split(2) stream
+    if (ttid == 0) {
+      int a = 0, b = n - 1;
+      if (t > 0) {
+        Rng pr{S.rng};
+        a = (int)pr.next_below((uint64_t)n);
+        b = (int)pr.next_below((uint64_t)(n - 1));
+        if (b >= a) ++b;
+        S.rng = pr.s;
+        // issued now, consumed after the scan: the load overlaps the pair work
+        thr_t = A.thr[(uint64_t)c * (A.iters + 1) + t];
+      }
+      S.a = a;
+      S.b = b;
+    }
+    team_sync<TW>(team);
+    const int pa = S.a, pb = S.b;
+    const int lo = t > 0 ? min(pa, pb) : 0, hi = t > 0 ? max(pa, pb) : n - 1;
+    for (int i = ttid; i < n; i += TW * 32) {
+      const int src = t == 0 ? i : (i == pa ? pb : (i == pb ? pa : i));
+      S.prop[i] = S.order[src];
+      S.pm[i] = S.cm[i];
+      S.pb[i] = S.cb[i];
+    }
+    team_sync<TW>(team);
+    // pair list (first warp of the team): positions lo..hi plus positions > hi
+    // whose best is an exact tie (their position-order tie-break may change)
+    if (twarp == 0) {
+      uint64_t bit[2];
+      bool take[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int p = 2 * lane + h;
+        bit[h] = p < n ? 1ull << S.prop[p] : 0ull;
+        take[h] = p < n && ((p >= lo && p <= hi) || (p > hi && (S.tied & bit[h])));
+      }
+      uint64_t incl = bit[0] | bit[1];
+      int cnt = (int)take[0] + (int)take[1];
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const uint64_t o = __shfl_up_sync(0xffffffffu, incl, off);
+        const int k = __shfl_up_sync(0xffffffffu, cnt, off);
+        if (lane >= off) {
+          incl |= o;
+          cnt += k;
+        }
+      }
+      int slot = cnt - (int)take[0] - (int)take[1];
+      const uint64_t pre0 = incl & ~(bit[0] | bit[1]);
+      const uint64_t pre[2] = {pre0, pre0 | bit[0]};
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int p = 2 * lane + h;
+        if (p >= n) continue;
+        const int v = S.prop[p];
+        S.ppos[v] = (uint8_t)p;
+        if (!take[h]) continue;
+        S.pv[slot] = (uint8_t)v;
+        S.pp[slot] = (uint8_t)p;
+        S.pc[slot] = nodes_to_cand(pre[h], v);
+        ++slot;
+      }
+      if (lane == 31) S.np = cnt;
+    }
+    team_sync<TW>(team);
+    const int np = S.np;
+    // ---- exact argmax of every rescanned row, one warp per pair
+    for (int q = twarp; q < np; q += TW) {
+      const int v = S.pv[q];
+      const PairOut o = pair_argmax(A, v, S.pp[q], S.pc[q], S.prop, S.ppos, s_bt, &walked, &enumerated);
+      if (lane == 0) {
+        S.pm[v] = cand_to_nodes(o.cm, v);
+        S.pb[v] = o.eff;
+        S.pt[q] = (uint8_t)o.tied;
+      }
+    }
+    pairs += np;
+    team_sync<TW>(team);
+    // ---- total in ascending node order (engine.cpp:95-96), tie bits, mh_accept
+    if (ttid == 0) {
+      double tot = 0.0;
+      for (int i = 0; i < n; ++i) tot += S.pb[i];
+      S.total = tot;
+      uint64_t tn = S.tied;
+      for (int q = 0; q < np; ++q) {
+        const uint64_t b = 1ull << S.pv[q];
+        tn = S.pt[q] ? (tn | b) : (tn & ~b);
+      }
+      S.tied_new = tn;
+      S.accept = t == 0 || thr_t < tot - S.cur_total;  // sampler.cpp:54-56
+    }
+    team_sync<TW>(team);
+    if (score_only) {
+      for (int i = ttid; i < n; i += TW * 32) {
+        A.out_masks[(uint64_t)c * n + i] = S.pm[i];
+        A.out_best[(uint64_t)c * n + i] = S.pb[i];
+      }
+      if (ttid == 0) A.out_total[c] = S.total;
+      break;
+    }
+    const double proposed = S.total;
+    const bool accepted = S.accept;
+    // ---- BestGraphTracker::update; every proposal is offered unless strict
+    if (twarp == 0 && (t == 0 || accepted || !A.strict))
+      tracker_offer_warp(tm, tt, A.K, n, S.pm, proposed, &S.tcount);
+    // ---- commit + trace row
+    if (accepted)
+      for (int i = ttid; i < n; i += TW * 32) {
+        S.cm[i] = S.pm[i];
+        S.cb[i] = S.pb[i];
+        S.order[i] = S.prop[i];
+      }
+    if (ttid == 0) {
+      if (accepted) {
+        S.cur_total = proposed;
+        S.tied = S.tied_new;
+        if (t > 0) ++S.acc;
+      }
+      if (t > 0) {
+        const uint64_t o = (uint64_t)c * A.iters + (t - 1);
+        A.tr_prop[o] = proposed;
+        A.tr_acc[o] = accepted ? 1 : 0;
+        A.tr_best[o] = tt[0];
+      }
+    }
+    team_sync<TW>(team);
+  }
+  if (!score_only) {
+    for (int i = ttid; i < n; i += TW * 32) A.final_order[(uint64_t)c * n + i] = S.order[i];
+    if (ttid == 0) {
+      A.final_score[c] = S.cur_total;
+      A.accepted[c] = S.acc;
+      A.tcount[c] = S.tcount;
+    }
+  }
+  if (lane == 0 && A.stat) {
+    atomicAdd(A.stat + 1, walked);
+    atomicAdd(A.stat + 2, enumerated);
+    if (twarp == 0) atomicAdd(A.stat, pairs);
+  }
+}
+
+}  // namespace bnmc_dev

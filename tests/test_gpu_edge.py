@@ -104,11 +104,13 @@ def test_exhaustive_n4_all_orders():
 
 
 @needs_ref
+@pytest.mark.parametrize("mode", [1, 2])
 @pytest.mark.parametrize("strict", [False, True])
-def test_chains_vs_reference_with_priors_and_strict(strict):
+def test_chains_vs_reference_with_priors_and_strict(strict, mode):
     cells, truth = ref.generate(12, 3, 500, [3] * 12, seed=5, tags=(1, 2, 3))
     pri = ref.synth_priors(12, truth, seed=5)
-    cfg = P.RunConfig(max_parents=3, iterations=800, track_top=4, strict_paper_tracker=strict)
+    cfg = P.RunConfig(max_parents=3, iterations=800, track_top=4, strict_paper_tracker=strict,
+                      scan_mode=mode)
     cache = P.ScoreCache.build(P.Dataset([3] * 12, cells), cfg, pri)
     rc = ref.Cache.build(cells, [3] * 12, 3)
     seeds = [3, 17, 99]
@@ -124,11 +126,12 @@ def test_chains_vs_reference_with_priors_and_strict(strict):
         assert many[c].accepted == r.accepted and many[c].final_score == r.final_score
 
 
-def test_tie_heavy_chain_matches_oracle():
+@pytest.mark.parametrize("mode", [1, 2])
+def test_tie_heavy_chain_matches_oracle(mode):
     """m tiny + gamma 1: many exact ties on fp32 AND fp64 keys, every scan cell
     goes through the exact tie resolution."""
     cells, cards = rand_instance(21, 10, 3, cmax=2)
-    cfg = P.RunConfig(max_parents=3, gamma=1.0, iterations=300)
+    cfg = P.RunConfig(max_parents=3, gamma=1.0, iterations=300, scan_mode=mode)
     cache = P.ScoreCache.build(P.Dataset(cards, cells), cfg)
     t = port.cache_build(cells, cards, 3, 1.0, 1.0)
     np.testing.assert_array_equal(cache.table(), t)
@@ -139,7 +142,8 @@ def test_tie_heavy_chain_matches_oracle():
         np.testing.assert_array_equal(r[c].tracker_masks, o["tracker_masks"])
 
 
-def test_set_priors_refold():
+@pytest.mark.parametrize("mode", [1, 2])
+def test_set_priors_refold(mode):
     cells, cards = rand_instance(22, 8, 200)
     cfg = P.RunConfig(max_parents=3)
     cache = P.ScoreCache.build(P.Dataset(cards, cells), cfg)
@@ -148,7 +152,7 @@ def test_set_priors_refold():
     perms = np.stack([rng.permutation(8) for _ in range(6)]).astype(np.int32)
     for k in range(3):
         pri = np.where(rng.random((8, 8)) < 0.3, rng.choice([0.0, 0.25, 0.75, 1.0], (8, 8)), 0.5)
-        masks, best, tot = P.OrderScorer(cache, pri).score_many(perms)
+        masks, best, tot = P.OrderScorer(cache, pri, scan_mode=mode).score_many(perms)
         for i in range(6):
             m, b, tt = port.score_order(t, 3, perms[i], pri)
             np.testing.assert_array_equal(masks[i], m)
@@ -198,15 +202,60 @@ def test_bnsc_upload_download_roundtrip(tmp_path, golden):
         port.index_of(20, 4, 3, 0b101)]
 
 
-def test_run_chains_many_chains_and_max():
+@pytest.mark.parametrize("mode", [1, 2])
+def test_run_chains_many_chains_and_max(mode):
     data, pri, cfg, _ = P.baseline_instance("cfg1")
     cache = P.ScoreCache.build(data, cfg, pri)
     cfg.iterations = 50
-    seeds = list(range(1, 65))
+    cfg.scan_mode = mode
+    seeds = list(range(1, 65 if mode == 1 else 1001))
     rs = P.run_chains(cache, pri, seeds, cfg)
     t = cache.table()
-    for c in (0, 31, 63):
+    for c in (0, 31, 63, len(seeds) - 1):
         o = port.run_mcmc(t, 3, 50, seeds[c], pri)
         np.testing.assert_array_equal(rs[c].trace_proposed, o["trace_proposed"])
-    with pytest.raises(P.UsageError):
-        P.run_chains(cache, pri, list(range(65)), cfg)
+        np.testing.assert_array_equal(rs[c].tracker_masks, o["tracker_masks"])
+    if mode == 1:
+        with pytest.raises(P.UsageError):
+            P.run_chains(cache, pri, list(range(65)), cfg)
+
+
+@pytest.mark.parametrize("mode", [1, 2])
+@pytest.mark.parametrize("seed,n,m,s", [(31, 1, 20, 3), (32, 2, 40, 1), (33, 7, 90, 0),
+                                        (34, 12, 300, 5), (35, 17, 500, 4), (36, 24, 800, 2)])
+def test_random_orders_both_scan_paths(seed, n, m, s, mode):
+    """Order scores of random instances with random priors, both scan paths
+    (full-row K2 and sorted walk / PST enumeration) vs the oracle's serial
+    score_order: masks, per-node bests and totals bit-exact."""
+    cells, cards = rand_instance(seed, n, m)
+    rng = np.random.default_rng(seed)
+    pri = np.where(rng.random((n, n)) < 0.3, rng.choice([0.0, 0.2, 0.8, 1.0], (n, n)), 0.5)
+    cfg = P.RunConfig(max_parents=s)
+    cache = P.ScoreCache.build(P.Dataset(cards, cells), cfg)
+    t = cache.table()
+    perms = np.stack([rng.permutation(n) for _ in range(16)]).astype(np.int32)
+    masks, best, tot = P.OrderScorer(cache, pri, scan_mode=mode).score_many(perms)
+    for i in range(16):
+        om, ob, ot = port.score_order(t, s, perms[i], pri)
+        np.testing.assert_array_equal(masks[i], om)
+        np.testing.assert_array_equal(best[i].view(np.uint64), ob.view(np.uint64))
+        assert tot[i] == ot
+
+
+@pytest.mark.parametrize("tw", [1, 2, 4, 8])
+def test_walk_team_sizes_identical(tw):
+    """The walk kernel's team size (warps per chain) changes only scheduling:
+    every chain's trace, tracker and final state equal the oracle's."""
+    data, pri, cfg, _ = P.baseline_instance("cfg2")
+    cache = P.ScoreCache.build(data, cfg, pri)
+    cfg.iterations, cfg.scan_mode, cfg.team_warps = 120, 2, tw
+    seeds = list(range(1, 38))  # not a multiple of the chains per CTA
+    rs = P.run_chains(cache, pri, seeds, cfg)
+    t = cache.table()
+    for c in (0, 5, 36):
+        o = port.run_mcmc(t, 4, 120, seeds[c], pri)
+        np.testing.assert_array_equal(rs[c].trace_proposed, o["trace_proposed"])
+        np.testing.assert_array_equal(rs[c].trace_best, o["trace_best"])
+        np.testing.assert_array_equal(rs[c].tracker_masks, o["tracker_masks"])
+        np.testing.assert_array_equal(rs[c].final_order, o["final_order"])
+        assert rs[c].accepted == o["accepted"]

@@ -52,22 +52,27 @@ def test_sampled_entries(name, golden):
                                   g["samp_val"].view(np.uint64))
 
 
+MODES = [1, 2]  # full-row scan (K2), sorted walk (K2W)
+
+
+@pytest.mark.parametrize("mode", MODES)
 @pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg3"])
-def test_order_scores_match_reference(name, golden):
+def test_order_scores_match_reference(name, mode, golden):
     data, pri, cfg = instance(name)
     g = golden(name)
     cache = P.ScoreCache.build(data, cfg, pri)
-    masks, best, tot = P.OrderScorer(cache, pri).score_many(g["orders"])
+    masks, best, tot = P.OrderScorer(cache, pri, scan_mode=mode).score_many(g["orders"])
     np.testing.assert_array_equal(masks, g["order_masks"])
     np.testing.assert_array_equal(tot.view(np.uint64), g["order_totals"].view(np.uint64))
 
 
+@pytest.mark.parametrize("mode", MODES)
 @pytest.mark.parametrize("name", ["cfg1", "cfg2"])
-def test_upload_path_scores(name, golden):
+def test_upload_path_scores(name, mode, golden):
     g = golden(name)
     data, pri, cfg = instance(name)
     cache = P.ScoreCache.from_table(g["table"], cfg, pri)
-    masks, best, tot = P.OrderScorer(cache, pri).score_many(g["orders"])
+    masks, best, tot = P.OrderScorer(cache, pri, scan_mode=mode).score_many(g["orders"])
     np.testing.assert_array_equal(masks, g["order_masks"])
     np.testing.assert_array_equal(tot, g["order_totals"])
     # per-node bests agree with the oracle's restatement
@@ -76,9 +81,11 @@ def test_upload_path_scores(name, golden):
         np.testing.assert_array_equal(best[i], ob)
 
 
+@pytest.mark.parametrize("mode", MODES)
 @pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg3"])
-def test_chain_matches_reference_trace(name, golden, golden_meta):
+def test_chain_matches_reference_trace(name, mode, golden, golden_meta):
     data, pri, cfg = instance(name)
+    cfg.scan_mode = mode
     g = golden(name)
     meta = golden_meta[name]
     cache = P.ScoreCache.build(data, cfg, pri)
@@ -94,7 +101,8 @@ def test_chain_matches_reference_trace(name, golden, golden_meta):
     assert r.final_score == meta["final_score"]
 
 
-def test_tie_fixture(golden_meta):
+@pytest.mark.parametrize("mode", MODES)
+def test_tie_fixture(mode, golden_meta):
     """all-zero table, the reference picks the first min(p,s)
     predecessors of the order (tie rule over POSITIONS, not cache indices)."""
     tf = golden_meta["tie_fixture"]
@@ -103,13 +111,15 @@ def test_tie_fixture(golden_meta):
     data = P.Dataset([3] * n, np.zeros((0, n), np.uint8))
     cache = P.ScoreCache.build(data, cfg)
     assert not cache.table().any()
-    sg = P.OrderScorer(cache).score(tf["perm"])
+    sg = P.OrderScorer(cache, scan_mode=mode).score(tf["perm"])
     assert [int(x) for x in sg.masks] == tf["masks"]
     assert sg.total == tf["total"]
 
 
-def test_multi_chain_equals_single_chains(golden):
+@pytest.mark.parametrize("mode", MODES)
+def test_multi_chain_equals_single_chains(mode, golden):
     data, pri, cfg = instance("cfg2")
+    cfg.scan_mode = mode
     cache = P.ScoreCache.build(data, cfg, pri)
     cfg.iterations = 300
     many = P.run_chains(cache, pri, [1, 2, 3, 4, 5], cfg)
@@ -121,7 +131,8 @@ def test_multi_chain_equals_single_chains(golden):
         assert many[c].accepted == one.accepted
 
 
-def test_cfg4_golden(golden, golden_meta):
+@pytest.mark.parametrize("mode", MODES)
+def test_cfg4_golden(mode, golden, golden_meta):
     """Headline scale: table SHA-256, 20 fixed orders and a 200-iteration chain
     identical to the unmodified reference (tests/golden/golden_cfg4.npz)."""
     meta = golden_meta["cfg4"]
@@ -130,10 +141,10 @@ def test_cfg4_golden(golden, golden_meta):
     assert sha(data.cells) == meta["cells_sha256"]
     cache = P.ScoreCache.build(data, cfg, pri)
     assert sha(cache.table()) == meta["table_sha256"]
-    masks, best, tot = P.OrderScorer(cache, pri).score_many(g["orders"])
+    masks, best, tot = P.OrderScorer(cache, pri, scan_mode=mode).score_many(g["orders"])
     np.testing.assert_array_equal(masks, g["order_masks"])
     np.testing.assert_array_equal(tot, g["order_totals"])
-    cfg.iterations, cfg.seed = meta["iterations"], meta["seed"]
+    cfg.iterations, cfg.seed, cfg.scan_mode = meta["iterations"], meta["seed"], mode
     r = P.run_mcmc(data, cfg, pri, prebuilt=cache)
     np.testing.assert_array_equal(r.trace_proposed, g["trace_proposed"])
     np.testing.assert_array_equal(r.tracker_masks, g["tracker_masks"])
