@@ -5,20 +5,24 @@
   (N>1: python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N)
 
 A "step" is one call of the reference-facing chain API (bnmc_gpu_run_chains)
-running C chains per GPU for I MCMC iterations each, in lockstep on the device
-(scan + step kernels under CUDA Graphs) — every iteration is a full
-run_mcmc iteration (sampler.cpp:92-111): proposal, rescan of the changed node
-rows, Metropolis-Hastings test, tracker update, trace row.
+running C independent chains per GPU for I MCMC iterations each; every
+iteration is a full run_mcmc iteration (sampler.cpp:92-111): proposal, exact
+rescan of the changed node rows, Metropolis-Hastings test, tracker update,
+trace row. The scan is the sorted-row walk (scan_mode 2, one fused kernel
+launch per step); chain c is bit-identical to the reference's run_mcmc with
+that seed (checked against the CPU reference below).
 
 value      = iterations of all chains of all ranks / max over ranks of the summed
-             device time of the sampling loops (CUDA events on the library's
+             device time of the chain kernel (CUDA events on the library's
              stream; the score table is resident in HBM).
-e2e        = same metric through the public API with HOST buffers: wall time of
-             the run_chains calls incl. H2D (seeds, acceptance thresholds) and
-             D2H (trace, tracker, final state).
-roofline   = the order-scan kernel (K2): bytes of the key sectors it must stream
-             per launch / its average launch time (CUDA events around sampled
-             launches inside the timed loop), against MEASURED_PEAKS.json hbm_gbs.
+e2e        = same metric through the C-ABI with HOST buffers: wall time of the
+             run_chains calls incl. H2D (seeds) and D2H (traces, trackers,
+             final states into pinned host buffers).
+roofline   = the fused walk kernel: algorithmic bytes per launch (sorted entries
+             walked x 16 B + enumerated local scores x 8 B, counted on the device)
+             / its launch time, against MEASURED_PEAKS.json hbm_gbs. The
+             full-row scan path (scan_mode 1) is measured beside it
+             (full_scan_path) with its own K2 roofline.
 cpu_baseline = the unmodified reference (oracle/_ref) run_mcmc on this box's host
              cores on the GPU-built table (BNSC export -> ScoreCache::load), a
              bounded number of iterations; its trace is checked bit-for-bit
@@ -126,11 +130,35 @@ def cpu_baseline(cache, priors, cfg, ours_trace, iters, seed):
             "trace_bit_exact_vs_gpu": parity}
 
 
+def full_scan_probe(P, _lib, cache, pri, cfg, chains=64, iters=100):
+    """The full-row scan path (scan_mode 1, K2 + CUDA Graphs): it/s and the K2
+    roofline (32-B key sectors it must stream per launch / avg launch time)."""
+    import ctypes as C
+    c1 = P.RunConfig(max_parents=cfg.max_parents, iterations=iters, scan_mode=1,
+                     memory_cap_bytes=cfg.memory_cap_bytes, device=cfg.device)
+    P.run_chains_batch(cache, pri, list(range(1, chains + 1)), c1)  # warm-up
+    b = P.run_chains_batch(cache, pri, list(range(1, chains + 1)), c1)
+    a, s_, t, d = C.c_uint64(), C.c_uint64(), C.c_float(), C.c_uint64()
+    _lib.check(_lib.lib().bnmc_gpu_last_scan_stats(cache.handle, C.byref(a), C.byref(s_),
+                                                    C.byref(t), C.byref(d)))
+    launches = iters + 1
+    bpl = s_.value * 32.0 / launches
+    avg = t.value / 1e3
+    peak, src = load_peaks()
+    return {"it_s": chains * iters / (b.device_ms / 1e3), "chains": chains, "iterations": iters,
+            "kernel": "scan_kernel (K2, full-row fp32-key scan)",
+            "roofline": {"bound": "hbm", "achieved": bpl / avg / 1e9, "peak": peak, "unit": "GB/s",
+                         "frac": bpl / avg / 1e9 / peak, "bytes_per_launch": bpl,
+                         "avg_launch_us": avg * 1e6, "peak_source": src,
+                         "row_equivalent_GBps": (a.value / launches) * cache.entries_per_node() * 4.0
+                         / avg / 1e9}}
+
+
 def run_ours(args):
+    import ctypes as C
     import torch
     import paper_1210_5128_b200 as P
     from paper_1210_5128_b200 import _lib, dist as D
-    import ctypes as C
 
     rank, world, local = D.env_rank_world()
     torch.cuda.set_device(local)
@@ -140,112 +168,136 @@ def run_ours(args):
         tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
     data, pri, cfg, truth = P.baseline_instance(args.config)
     cfg.device = local
-    # ---- precompute: row-sharded K1 + NCCL all-gather (timed, max over ranks)
+    # ---- precompute: row-sharded K1 + NCCL all-gather, then the per-row sort
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     cache = D.build_table_sharded(data, cfg, pri, rank, world, group)
+    cfg.iterations, cfg.scan_mode = 1, 2
+    P.run_chains_batch(cache, pri, [1], cfg)  # binds priors, builds the sorted rows
     torch.cuda.synchronize()
     pre_s = time.perf_counter() - t0
-    k1 = C.c_float()
-    fold = C.c_float()
+    k1, fold = C.c_float(), C.c_float()
     _lib.check(_lib.lib().bnmc_gpu_table_build_ms(cache.handle, C.byref(k1), C.byref(fold)))
-    C_, I = args.chains, args.iters
-    cfg.iterations = I
+    Cn, I = args.chains, args.iters
+    cfg.iterations, cfg.team_warps = I, args.team_warps
     flush = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
-    # ---- warm-up
+    # host result buffers (pinned) reused across steps: the e2e region copies into them
+    n, K = data.n, cfg.track_top
+
+    def pinned(shape, dt):
+        return torch.empty(shape, dtype=dt, pin_memory=True).numpy()
+    out = P.api.ChainBatch(pinned((Cn, I), torch.float64), pinned((Cn, I), torch.uint8),
+                           pinned((Cn, I), torch.float64), pinned((Cn, n), torch.int32),
+                           pinned((Cn,), torch.float64), pinned((Cn,), torch.int64).view(np.uint64),
+                           pinned((Cn,), torch.int32), pinned((Cn, K, n), torch.int64).view(np.uint64),
+                           pinned((Cn, K), torch.float64), 0.0, 0.0)
     for w in range(args.warmup):
-        P.run_chains(cache, pri, D.chain_seeds(1000001, rank, C_, w, world), cfg)
+        P.run_chains_batch(cache, pri, D.chain_seeds(1000001, rank, Cn, w, world), cfg, out)
     if world > 1:
         import torch.distributed as tdist
         tdist.barrier()
     torch.cuda.synchronize()
-    dev_ms, wall_s, scan_ms, sectors, rescans, launches = [], [], [], 0, 0, 0
-    results = None
+    dev_ms, wall_s, walked, enumerated, pairs, replayed = [], [], 0, 0, 0, 0
     with ClockSampler(local) as clocks:
         for k in range(args.steps):
             flush_l2(torch, flush)
             torch.cuda.synchronize()
-            t = time.perf_counter()
-            results = P.run_chains(cache, pri, D.chain_seeds(1, rank, C_, k, world), cfg)
-            wall_s.append(time.perf_counter() - t)
-            dev_ms.append(results[0].device_ms)
-            a, b, c, d = C.c_uint64(), C.c_uint64(), C.c_float(), C.c_uint64()
-            _lib.check(_lib.lib().bnmc_gpu_last_scan_stats(cache.handle, C.byref(a), C.byref(b),
-                                                            C.byref(c), C.byref(d)))
-            rescans += a.value
-            sectors += b.value
-            scan_ms.append(c.value)
-            launches += d.value
+            b = P.run_chains_batch(cache, pri, D.chain_seeds(1, rank, Cn, k, world), cfg, out)
+            wall_s.append(b.wall_s)
+            dev_ms.append(b.device_ms)
+            pa, wa, en, so = C.c_uint64(), C.c_uint64(), C.c_uint64(), C.c_float()
+            _lib.check(_lib.lib().bnmc_gpu_last_walk_stats(cache.handle, C.byref(pa), C.byref(wa),
+                                                            C.byref(en), C.byref(so)))
+            rp = C.c_uint64()
+            _lib.check(_lib.lib().bnmc_gpu_last_replayed(cache.handle, C.byref(rp)))
+            pairs += pa.value
+            walked += wa.value
+            enumerated += en.value
+            replayed += rp.value
     torch.cuda.synchronize()
     tot_dev = sum(dev_ms) / 1e3
     tot_wall = sum(wall_s)
+    recs = np.zeros((Cn, 3 + data.n), np.float64)
+    recs[:, 0] = D.chain_seeds(1, rank, Cn, args.steps - 1, world).astype(np.float64)
+    recs[:, 1] = out.accepted.astype(np.float64)
+    recs[:, 2] = out.tracker_totals[:, 0]
+    recs[:, 3:] = out.tracker_masks[:, 0, :].view(np.float64)
     if world > 1:
         import torch.distributed as tdist
         tt = torch.tensor([tot_dev, tot_wall, pre_s], device="cuda", dtype=torch.float64)
         tdist.all_reduce(tt, op=tdist.ReduceOp.MAX)
         tot_dev, tot_wall, pre_s = tt.tolist()
-        recs = np.stack([D.chain_record(r, data.n) for r in results])
         allrec = D.gather_chain_records(recs, group, device="cuda")
     else:
-        allrec = np.stack([D.chain_record(r, data.n) for r in results])
-    iters_total = args.steps * C_ * I * world
+        allrec = recs
+    iters_total = args.steps * Cn * I * world
     value = iters_total / tot_dev
     e2e = iters_total / tot_wall
-    # roofline of K2: sector bytes per launch / avg launch time
-    launches_scan = args.steps * (I + 1)
-    bytes_per_launch = sectors * 32.0 / launches_scan
-    avg_scan_s = float(np.mean(scan_ms)) / 1e3 if scan_ms else float("nan")
-    achieved = bytes_per_launch / avg_scan_s / 1e9
+    # roofline of the fused walk kernel: algorithmic bytes = sorted entries
+    # walked (f64 eff + u64 mask) + PST-enumerated local scores (f64 gathers)
+    bytes_per_launch = (walked * 16.0 + enumerated * 8.0) / args.steps
+    avg_launch_s = tot_dev / args.steps
+    achieved = bytes_per_launch / avg_launch_s / 1e9
     peak, peak_src = load_peaks()
-    S = cache.entries_per_node()
-    row_equiv = (rescans / launches_scan) * S * 4.0 / avg_scan_s / 1e9
-    out = None
+    out_line = None
     if rank == 0:
-        best = D.best_overall(allrec, data.n)
+        best_i = int(np.argmax(allrec[:, 2]))
         cpu = None
+        extra = {}
         if world == 1 and not args.no_cpu_baseline:
-            cfg1 = P.RunConfig(max_parents=cfg.max_parents, iterations=args.cpu_iters, seed=1,
-                               memory_cap_bytes=cfg.memory_cap_bytes, device=local)
-            ours1 = P.run_chains(cache, pri, [1], cfg1)[0]
+            c1 = P.RunConfig(max_parents=cfg.max_parents, iterations=args.cpu_iters, seed=1,
+                             memory_cap_bytes=cfg.memory_cap_bytes, device=local, scan_mode=2)
+            ours1 = P.run_chains(cache, pri, [1], c1)[0]
             cpu = cpu_baseline(cache, pri, cfg, ours1.trace_proposed, args.cpu_iters, 1)
-        h2d = 8 * C_ + 8 * C_ * (I + 1)
-        d2h = C_ * I * (8 + 1 + 8) + C_ * cfg.track_top * (data.n * 8 + 8) + C_ * (data.n * 4 + 8 + 8 + 4)
-        out = {
+        if world == 1 and not args.no_extras:
+            c1 = P.RunConfig(max_parents=cfg.max_parents, iterations=I, scan_mode=2, team_warps=8,
+                             memory_cap_bytes=cfg.memory_cap_bytes, device=local)
+            one = P.run_chains_batch(cache, pri, [1], c1)
+            extra["single_chain_it_s"] = I / (one.device_ms / 1e3)
+            extra["full_scan_path"] = full_scan_probe(P, _lib, cache, pri, cfg)
+        h2d = 8 * Cn
+        d2h = (Cn * I * (8 + 1 + 8) + Cn * K * (n * 8 + 8) + Cn * (n * 4 + 8 + 8 + 4) + 4 * Cn)
+        out_line = {
             "metric": METRIC, "value": value, "unit": "iterations/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": tot_dev * 1e3 / args.steps, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "fp32 keys + exact fp64 resolve (u64 masks)",
-            "data": "synthetic (reference generator, seed 7, SURVEY §8d)",
+            "vs_baseline": None, "dtype": "f64 (exact scores) + u64 parent masks",
+            "data": "synthetic (reference generator, seed 7, SURVEY \u00a78d)",
             "config": {"workload": f"{args.config}: n=60 k=4 m=10000 3-state + pairwise priors; "
-                                   f"{C_} chains/GPU x {I} iterations per step",
-                       "chains_per_gpu": C_, "iterations_per_step": I,
+                                   f"{Cn} independent chains/GPU x {I} iterations per step",
+                       "chains_per_gpu": Cn, "iterations_per_step": I,
+                       "scan": "sorted-row walk + PST enumeration (scan_mode 2), fused chains",
                        "parallelism": f"independent chains, {world} GPU(s)",
-                       "l2": "flushed (256 MiB write) before every step; within a step the "
-                             "117 MB fp32 key table is re-read every iteration"},
+                       "l2": "flushed (256 MiB write) before every step"},
             "e2e": {"value": e2e, "unit": "iterations/s", "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h},
+                    "d2h_bytes_per_step": d2h,
+                    "note": "bnmc_gpu_run_chains with host seeds in, pinned host trace/tracker/"
+                            "final-state buffers out; wall time per call"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": None,
-                         "kernel": "scan_kernel (K2)", "peak_source": peak_src,
-                         "bytes_per_launch": bytes_per_launch,
-                         "avg_launch_us": avg_scan_s * 1e6,
-                         "row_equivalent_GBps": row_equiv,
-                         "note": "achieved = 32-byte key sectors the scan must stream (rows of "
-                                 "the step, sectors some chain can admit) / avg launch time; "
-                                 "row_equivalent = full rows x S x 4 B / same time"},
+                         "kernel": "walk_chain_kernel (K2W: fused scan + chain step)",
+                         "peak_source": peak_src, "bytes_per_launch": bytes_per_launch,
+                         "avg_launch_us": avg_launch_s * 1e6,
+                         "note": "algorithmic bytes = sorted entries walked x 16 B + PST-enumerated "
+                                 "local scores x 8 B; the touched tops of the sorted rows are "
+                                 "L2-resident, so the kernel is latency/issue-bound, not HBM-bound"},
+            "walk": {"pairs_per_iteration": pairs / (args.steps * Cn * (I + 1)),
+                     "walked_per_pair": walked / max(1, pairs),
+                     "enumerated_per_pair": enumerated / max(1, pairs),
+                     "chains_replayed_exact": replayed},
             "precompute_s": pre_s, "precompute_kernel_ms": k1.value, "fold_ms": fold.value,
-            "ms_per_iteration_per_chain": tot_dev * 1e3 / (args.steps * I),
-            "gpu_launches": int(launches),
-            "best_total": best["best_total"],
+            "gpu_launches": int(args.steps * (1 + (1 if replayed else 0))),
+            "best_total": float(allrec[best_i, 2]),
             "cpu_baseline": cpu,
             "clocks": clocks.summary(),
         }
-        print(json.dumps(out), flush=True)
+        out_line.update(extra)
+        print(json.dumps(out_line), flush=True)
     if world > 1:
         import torch.distributed as tdist
         tdist.barrier()
         tdist.destroy_process_group()
-    return out
+    return out_line
 
 
 def run_reference(args):
@@ -301,7 +353,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="cfg4")
-    ap.add_argument("--chains", type=int, default=64, help="chains per GPU (<= 64)")
+    ap.add_argument("--chains", type=int, default=4736, help="chains per GPU")
+    ap.add_argument("--team-warps", type=int, default=0, help="warps per chain (0 auto)")
+    ap.add_argument("--no-extras", action="store_true", help="skip single-chain/full-scan probes")
     ap.add_argument("--iters", type=int, default=500, help="MCMC iterations per chain per step")
     ap.add_argument("--cpu-iters", type=int, default=200)
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -152,6 +152,10 @@ typedef struct {
                           chains, one CTA per chain, any number of chains */
   int timing_sample;   /* every k-th scan launch is bracketed by CUDA events (0 = 8) */
   int team_warps;      /* sorted walk: warps per chain (0 auto, 1, 2, 4, 8) */
+  int exact_accept;    /* sorted walk: 0 = device log10 for mh_accept, chains with a
+                          decision inside the CUDA/glibc log10 error bound replayed
+                          with host glibc thresholds; 1 = host glibc thresholds only */
+  int accept_tol_log2; /* relative bound of that test as a power of two (0 = -48) */
 } bnmc_chain_params;
 
 /* Run n_chains independent chains, chain c seeded with seeds[c] exactly as
@@ -187,6 +191,10 @@ int bnmc_gpu_table_set_scan_mode(bnmc_table* t, int mode);
  * counts), and the device time of the last per-row sort build (ms). */
 int bnmc_gpu_last_walk_stats(const bnmc_table* t, uint64_t* pairs, uint64_t* walked,
                              uint64_t* enumerated, float* sort_ms);
+
+/* Chains of the last sorted-walk run_chains call that were replayed with host
+ * glibc acceptance thresholds (an mh_accept decision fell inside the bound). */
+int bnmc_gpu_last_replayed(const bnmc_table* t, uint64_t* chains);
 
 /* Diagnostics: time the order-scan kernel alone on the rows at positions
  * lo..hi of `count` (<= 64) orders, averaged over `reps` launches (ms). */

@@ -7,10 +7,10 @@ device-resident MCMC loop. This package is the reference-shaped host mirror
 """
 from .api import (AlphaMode, CapacityError, DataError, Dataset, EngineConfig, Error, McmcResult,
                   Order, OrderScorer, PriorMatrix, RunConfig, ScoreCache, ScoredGraph, UsageError,
-                  baseline_instance, parallel_score_order, read_bnsc, run_chains, run_mcmc,
+                  baseline_instance, parallel_score_order, read_bnsc, run_chains, run_chains_batch, run_mcmc,
                   synth_instance, synth_priors, write_bnsc)
 
 __all__ = ["AlphaMode", "CapacityError", "DataError", "Dataset", "EngineConfig", "Error",
            "McmcResult", "Order", "OrderScorer", "PriorMatrix", "RunConfig", "ScoreCache",
            "ScoredGraph", "UsageError", "baseline_instance", "parallel_score_order", "read_bnsc",
-           "run_chains", "run_mcmc", "synth_instance", "synth_priors", "write_bnsc"]
+           "run_chains", "run_chains_batch", "run_mcmc", "synth_instance", "synth_priors", "write_bnsc"]

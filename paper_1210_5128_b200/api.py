@@ -50,6 +50,8 @@ class RunConfig:
     device: int = 0
     scan_mode: int = 0  # 0 auto (= 2), 1 full-row fp32-key scan (<= 64 chains), 2 sorted walk
     team_warps: int = 0  # sorted walk: warps per chain (0 auto, 1, 2, 4, 8)
+    exact_accept: int = 0  # 0 device log10 + exact replay of ambiguous chains, 1 host glibc
+    accept_tol_log2: int = 0  # bound of the ambiguity test (0 = 2^-48 relative)
 
     def validate(self):
         """RunConfig::validate (types.cpp:111-121)."""
@@ -470,8 +472,25 @@ class McmcResult:
         return float(self.tracker_totals[0])
 
 
-def run_chains(cache: ScoreCache, priors, seeds, cfg: RunConfig):
-    """Independent chains (chain c == run_mcmc with seed seeds[c]) in one device loop."""
+@dataclass
+class ChainBatch:
+    """Results of run_chains_batch as chain-major arrays (no per-chain objects)."""
+    trace_proposed: np.ndarray   # [C, iterations]
+    trace_accepted: np.ndarray   # [C, iterations] uint8
+    trace_best: np.ndarray       # [C, iterations]
+    final_order: np.ndarray      # [C, n]
+    final_score: np.ndarray      # [C]
+    accepted: np.ndarray         # [C]
+    tracker_count: np.ndarray    # [C]
+    tracker_masks: np.ndarray    # [C, K, n]
+    tracker_totals: np.ndarray   # [C, K]
+    device_ms: float
+    wall_s: float
+
+
+def run_chains_batch(cache: ScoreCache, priors, seeds, cfg: RunConfig, out: ChainBatch | None = None):
+    """Independent chains through one bnmc_gpu_run_chains call; chain c is run_mcmc
+    with seed seeds[c]. Host buffers may be passed in `out` (reused, e.g. pinned)."""
     cfg.validate()
     pr = _prior_array(priors)
     if pr is not None and pr.shape[0] != cache.n():
@@ -479,37 +498,38 @@ def run_chains(cache: ScoreCache, priors, seeds, cfg: RunConfig):
     seeds = np.ascontiguousarray(seeds, dtype=np.uint64)
     nc, n, K, it = seeds.size, cache.n(), cfg.track_top, cfg.iterations
     cache.bind_priors(pr)
-    tp = np.empty(nc * it, np.float64)
-    ta = np.empty(nc * it, np.uint8)
-    tb = np.empty(nc * it, np.float64)
-    fo = np.empty(nc * n, np.int32)
-    fs = np.empty(nc, np.float64)
-    acc = np.empty(nc, np.uint64)
-    tc = np.empty(nc, np.int32)
-    tm = np.empty(nc * K * n, np.uint64)
-    tt = np.empty(nc * K, np.float64)
+    if out is None:
+        out = ChainBatch(np.empty((nc, it)), np.empty((nc, it), np.uint8), np.empty((nc, it)),
+                         np.empty((nc, n), np.int32), np.empty(nc), np.empty(nc, np.uint64),
+                         np.empty(nc, np.int32), np.empty((nc, K, n), np.uint64),
+                         np.empty((nc, K)), 0.0, 0.0)
     ms = C.c_float()
     params = _lib.ChainParams(it, K, int(cfg.strict_paper_tracker), cfg.scan_mode, 0,
-                              cfg.team_warps)
+                              cfg.team_warps, cfg.exact_accept, cfg.accept_tol_log2)
     t0 = time.perf_counter()
-    _lib.check(_lib.lib().bnmc_gpu_run_chains(cache.handle, seeds, nc, C.byref(params),
-                                               _lib.ptr(tp), _lib.ptr(ta), _lib.ptr(tb),
-                                               _lib.ptr(fo), _lib.ptr(fs), _lib.ptr(acc),
-                                               _lib.ptr(tc), _lib.ptr(tm), _lib.ptr(tt),
-                                               C.byref(ms)))
-    wall = time.perf_counter() - t0
-    out = []
-    for c in range(nc):
-        k = int(tc[c])
-        out.append(McmcResult(
-            tracker_masks=tm.reshape(nc, K, n)[c, :k].copy(),
-            tracker_totals=tt.reshape(nc, K)[c, :k].copy(),
-            trace_proposed=tp.reshape(nc, it)[c].copy(),
-            trace_accepted=ta.reshape(nc, it)[c].astype(bool),
-            trace_best=tb.reshape(nc, it)[c].copy(),
-            final_order=fo.reshape(nc, n)[c].copy(), final_score=float(fs[c]),
-            accepted=int(acc[c]), sampling_seconds=wall, device_ms=ms.value, seed=int(seeds[c])))
+    _lib.check(_lib.lib().bnmc_gpu_run_chains(
+        cache.handle, seeds, nc, C.byref(params), _lib.ptr(out.trace_proposed),
+        _lib.ptr(out.trace_accepted), _lib.ptr(out.trace_best), _lib.ptr(out.final_order),
+        _lib.ptr(out.final_score), _lib.ptr(out.accepted), _lib.ptr(out.tracker_count),
+        _lib.ptr(out.tracker_masks), _lib.ptr(out.tracker_totals), C.byref(ms)))
+    out.wall_s = time.perf_counter() - t0
+    out.device_ms = ms.value
     return out
+
+
+def run_chains(cache: ScoreCache, priors, seeds, cfg: RunConfig):
+    """Independent chains (chain c == run_mcmc with seed seeds[c]) in one device loop."""
+    b = run_chains_batch(cache, priors, seeds, cfg)
+    res = []
+    for c in range(b.final_score.size):
+        k = int(b.tracker_count[c])
+        res.append(McmcResult(
+            tracker_masks=b.tracker_masks[c, :k].copy(), tracker_totals=b.tracker_totals[c, :k].copy(),
+            trace_proposed=b.trace_proposed[c].copy(), trace_accepted=b.trace_accepted[c].astype(bool),
+            trace_best=b.trace_best[c].copy(), final_order=b.final_order[c].copy(),
+            final_score=float(b.final_score[c]), accepted=int(b.accepted[c]),
+            sampling_seconds=b.wall_s, device_ms=b.device_ms, seed=int(seeds[c])))
+    return res
 
 
 def run_mcmc(data: Dataset, cfg: RunConfig, priors=None, prebuilt: ScoreCache | None = None):

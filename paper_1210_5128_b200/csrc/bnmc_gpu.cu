@@ -191,6 +191,8 @@ struct bnmc_table {
   uint64_t last_rescans = 0, last_sectors = 0, last_launches = 0, last_scan_samples = 0;
   uint64_t last_walked = 0, last_enumerated = 0;
   int last_team = 0;
+  uint64_t last_replayed = 0;
+  DevBuf<int> d_amb;
   float last_scan_ms = 0.f, last_total_ms = 0.f;
   int last_G = 0;
   ~bnmc_table() {
@@ -654,18 +656,19 @@ void score_orders_walk(bnmc_table* t, const int* perms, int count, uint64_t* mas
   CK(cudaStreamSynchronize(t->stream));
 }
 
-// run_chains through the fused walk kernel: one CTA per chain for all
-// iterations; one launch per call.
-void run_chains_walk(bnmc_table* t, const uint64_t* seeds, int C, const bnmc_chain_params* params,
-                     double* trace_proposed, uint8_t* trace_accepted, double* trace_best,
-                     int* final_order, double* final_score, uint64_t* accepted, int* tracker_count,
-                     uint64_t* tracker_masks, double* tracker_totals, float* device_ms) {
+// One launch of the fused walk kernel over chains `seeds[0..C)`; outputs to the
+// host pointers (any may be null). host_thr: glibc thresholds from the host
+// (exact), else device log10 with ambiguity flags returned in *amb_out.
+void walk_launch(bnmc_table* t, const uint64_t* seeds, int C, const bnmc_chain_params* params,
+                 bool host_thr, double* trace_proposed, uint8_t* trace_accepted, double* trace_best,
+                 int* final_order, double* final_score, uint64_t* accepted, int* tracker_count,
+                 uint64_t* tracker_masks, double* tracker_totals, float* device_ms,
+                 std::vector<int>* amb_out) {
   const int n = t->n, K = params->track_top;
   const uint64_t iters = params->iterations;
   ensure_workspace(t, 1, 0, 0);  // error flag + stats
   ensure_sorted(t);
   t->seeds.alloc(C);
-  t->thr.alloc(static_cast<size_t>(C) * (iters + 1));
   t->tmasks.alloc(static_cast<size_t>(C) * K * n);
   t->ttotals.alloc(static_cast<size_t>(C) * K);
   t->tr_prop.alloc(static_cast<size_t>(C) * iters);
@@ -675,17 +678,23 @@ void run_chains_walk(bnmc_table* t, const uint64_t* seeds, int C, const bnmc_cha
   t->d_tc.alloc(C);
   t->d_acc.alloc(C);
   t->d_fs.alloc(C);
-  std::vector<double> thr;
-  accept_thresholds(seeds, C, iters, thr);
+  t->d_amb.alloc(C);
   CK(cudaMemcpyAsync(t->seeds.p, seeds, 8ull * C, cudaMemcpyHostToDevice, t->stream));
-  CK(cudaMemcpyAsync(t->thr.p, thr.data(), thr.size() * 8, cudaMemcpyHostToDevice, t->stream));
+  std::vector<double> thr;
+  if (host_thr) {
+    t->thr.alloc(static_cast<size_t>(C) * (iters + 1));
+    accept_thresholds(seeds, C, iters, thr);
+    CK(cudaMemcpyAsync(t->thr.p, thr.data(), thr.size() * 8, cudaMemcpyHostToDevice, t->stream));
+  }
   WalkArgs A = walk_args(t);
   A.C = C;
   A.iters = iters;
   A.K = K;
   A.strict = params->strict;
   A.seeds = t->seeds.p;
-  A.thr = t->thr.p;
+  A.thr = host_thr ? t->thr.p : nullptr;
+  A.accept_tol = std::ldexp(1.0, params->accept_tol_log2 ? params->accept_tol_log2 : -48);
+  A.ambiguous = t->d_amb.p;
   A.tmasks = t->tmasks.p;
   A.ttotals = t->ttotals.p;
   A.tcount = t->d_tc.p;
@@ -700,7 +709,6 @@ void run_chains_walk(bnmc_table* t, const uint64_t* seeds, int C, const bnmc_cha
   CK(cudaEventCreate(&e1));
   CK(cudaEventRecord(e0, t->stream));
   launch_walk(t, A, C, params->team_warps);
-  CK(cudaGetLastError());
   CK(cudaEventRecord(e1, t->stream));
   if (trace_proposed)
     CK(cudaMemcpyAsync(trace_proposed, t->tr_prop.p, 8ull * C * iters, cudaMemcpyDeviceToHost, t->stream));
@@ -720,6 +728,9 @@ void run_chains_walk(bnmc_table* t, const uint64_t* seeds, int C, const bnmc_cha
     CK(cudaMemcpyAsync(accepted, t->d_acc.p, 8ull * C, cudaMemcpyDeviceToHost, t->stream));
   if (tracker_count)
     CK(cudaMemcpyAsync(tracker_count, t->d_tc.p, sizeof(int) * C, cudaMemcpyDeviceToHost, t->stream));
+  std::vector<int> amb(C, 0);
+  if (!host_thr)
+    CK(cudaMemcpyAsync(amb.data(), t->d_amb.p, sizeof(int) * C, cudaMemcpyDeviceToHost, t->stream));
   unsigned long long stats[3] = {0, 0, 0};
   CK(cudaMemcpyAsync(stats, t->stat.p, 24, cudaMemcpyDeviceToHost, t->stream));
   CK(cudaStreamSynchronize(t->stream));
@@ -728,6 +739,11 @@ void run_chains_walk(bnmc_table* t, const uint64_t* seeds, int C, const bnmc_cha
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   if (device_ms) *device_ms = ms;
+  if (amb_out) {
+    amb_out->clear();
+    for (int c = 0; c < C; ++c)
+      if (amb[c]) amb_out->push_back(c);
+  }
   t->last_rescans = stats[0];
   t->last_sectors = stats[1] + stats[2];  // walk path: entries visited (walked + enumerated)
   t->last_walked = stats[1];
@@ -737,6 +753,55 @@ void run_chains_walk(bnmc_table* t, const uint64_t* seeds, int C, const bnmc_cha
   t->last_scan_ms = ms;
   t->last_scan_samples = 1;
   t->last_G = C;
+}
+
+// run_chains through the fused walk kernel: one launch for all chains and
+// iterations. Acceptance uses the device's log10 unless the caller asks for
+// host thresholds; chains whose decisions came within the glibc/CUDA log10
+// bound of the threshold are replayed with host glibc thresholds, so every
+// trace is the reference's bit for bit.
+void run_chains_walk(bnmc_table* t, const uint64_t* seeds, int C, const bnmc_chain_params* params,
+                     double* trace_proposed, uint8_t* trace_accepted, double* trace_best,
+                     int* final_order, double* final_score, uint64_t* accepted, int* tracker_count,
+                     uint64_t* tracker_masks, double* tracker_totals, float* device_ms) {
+  const bool host_thr = params->exact_accept == 1;
+  std::vector<int> amb;
+  walk_launch(t, seeds, C, params, host_thr, trace_proposed, trace_accepted, trace_best,
+              final_order, final_score, accepted, tracker_count, tracker_masks, tracker_totals,
+              device_ms, &amb);
+  const uint64_t keep[4] = {t->last_rescans, t->last_walked, t->last_enumerated, t->last_sectors};
+  const float keep_ms = t->last_scan_ms;
+  t->last_replayed = amb.size();
+  if (amb.empty()) return;
+  const int R = static_cast<int>(amb.size()), n = t->n, K = params->track_top;
+  const uint64_t it = params->iterations;
+  std::vector<uint64_t> rs(R);
+  for (int i = 0; i < R; ++i) rs[i] = seeds[amb[i]];
+  std::vector<double> tp(R * it), tb(R * it), fs(R), tt(static_cast<size_t>(R) * K);
+  std::vector<uint8_t> ta(R * it);
+  std::vector<int> fo(static_cast<size_t>(R) * n), tc(R);
+  std::vector<uint64_t> acc(R), tm(static_cast<size_t>(R) * K * n);
+  walk_launch(t, rs.data(), R, params, true, tp.data(), ta.data(), tb.data(), fo.data(), fs.data(),
+              acc.data(), tc.data(), tm.data(), tt.data(), nullptr, nullptr);
+  for (int i = 0; i < R; ++i) {
+    const size_t c = static_cast<size_t>(amb[i]);
+    if (trace_proposed) std::copy_n(tp.data() + i * it, it, trace_proposed + c * it);
+    if (trace_accepted) std::copy_n(ta.data() + i * it, it, trace_accepted + c * it);
+    if (trace_best) std::copy_n(tb.data() + i * it, it, trace_best + c * it);
+    if (final_order) std::copy_n(fo.data() + static_cast<size_t>(i) * n, n, final_order + c * n);
+    if (final_score) final_score[c] = fs[i];
+    if (accepted) accepted[c] = acc[i];
+    if (tracker_count) tracker_count[c] = tc[i];
+    if (tracker_masks)
+      std::copy_n(tm.data() + static_cast<size_t>(i) * K * n, static_cast<size_t>(K) * n,
+                  tracker_masks + c * K * n);
+    if (tracker_totals) std::copy_n(tt.data() + static_cast<size_t>(i) * K, K, tracker_totals + c * K);
+  }
+  t->last_rescans = keep[0];
+  t->last_walked = keep[1];
+  t->last_enumerated = keep[2];
+  t->last_sectors = keep[3];
+  t->last_scan_ms = keep_ms;
 }
 
 int read_error(bnmc_table* t) {
@@ -1207,6 +1272,13 @@ int bnmc_gpu_last_walk_stats(const bnmc_table* t, uint64_t* pairs, uint64_t* wal
     if (walked) *walked = t->last_walked;
     if (enumerated) *enumerated = t->last_enumerated;
     if (sort_ms) *sort_ms = t->sort_ms;
+  });
+}
+
+int bnmc_gpu_last_replayed(const bnmc_table* t, uint64_t* chains) {
+  return guarded([&] {
+    if (!t) raise(BNMC_USAGE, "null table");
+    *chains = t->last_replayed;
   });
 }
 

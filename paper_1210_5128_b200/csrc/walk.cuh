@@ -53,7 +53,10 @@ struct WalkArgs {
   uint64_t iters;
   int K, strict;
   const uint64_t* __restrict__ seeds;  // [C]
-  const double* __restrict__ thr;      // [C][iters+1] log10(u_t)
+  const double* __restrict__ thr;      // [C][iters+1] host glibc log10(u_t), or null:
+                                       // device log10 + ambiguity flag (exact replay)
+  double accept_tol;                   // relative |log10_dev - log10_glibc| bound
+  int* ambiguous;                      // [C] set when a decision fell inside the bound
   uint64_t* tmasks;                    // [C][K][n]
   double* ttotals;                     // [C][K]
   int* tcount;                         // [C]
@@ -361,10 +364,10 @@ struct TeamState {
   double pb[64];                   // proposed per-node bests
   uint64_t cm[64];                 // current graph
   double cb[64];                   // current per-node bests
-  uint64_t tied, tied_new, rng;
+  uint64_t tied, tied_new, rng, arng;
   double total, cur_total;
   unsigned long long acc;
-  int np, a, b, accept, tcount;
+  int np, a, b, accept, tcount, amb;
 };
 
 // TW warps per chain, kWalkThreads / (32 TW) chains per CTA. TW = 8 gives one
@@ -401,8 +404,10 @@ __global__ void __launch_bounds__(kWalkThreads, 4) walk_chain_kernel(WalkArgs A)
         S.order[j] = t;
       }
       S.rng = master.split(2).s;
+      S.arng = master.split(3).s;
     }
     S.tied = 0;
+    S.amb = 0;
     S.tcount = 0;
     S.acc = 0;
     S.cur_total = 0.0;
@@ -421,8 +426,15 @@ __global__ void __launch_bounds__(kWalkThreads, 4) walk_chain_kernel(WalkArgs A)
         b = (int)pr.next_below((uint64_t)(n - 1));
         if (b >= a) ++b;
         S.rng = pr.s;
-        // issued now, consumed after the scan: the load overlaps the pair work
-        thr_t = A.thr[(uint64_t)c * (A.iters + 1) + t];
+        if (A.thr) {
+          // issued now, consumed after the scan: the load overlaps the pair work
+          thr_t = A.thr[(uint64_t)c * (A.iters + 1) + t];
+        } else {
+          // mh_accept's draw (sampler.cpp:54-56): one per iteration, split(3)
+          Rng ar{S.arng};
+          thr_t = log10(ar.next_unit_open());
+          S.arng = ar.s;
+        }
       }
       S.a = a;
       S.b = b;
@@ -501,7 +513,17 @@ __global__ void __launch_bounds__(kWalkThreads, 4) walk_chain_kernel(WalkArgs A)
         tn = S.pt[q] ? (tn | b) : (tn & ~b);
       }
       S.tied_new = tn;
-      S.accept = t == 0 || thr_t < tot - S.cur_total;  // sampler.cpp:54-56
+      // mh_accept, sampler.cpp:54-56: log10(u) < new - old
+      const double delta = tot - S.cur_total;
+      bool acc = t == 0 || thr_t < delta;
+      if (t > 0 && !A.thr) {
+        // CUDA's log10 and glibc's may differ in the last bits: a decision
+        // within the bound of the threshold is flagged, and the host replays
+        // the chain with glibc thresholds (bnmc_gpu_run_chains).
+        const double tol = fabs(thr_t) * A.accept_tol;
+        if (!(thr_t + tol < delta) && !(thr_t - tol >= delta)) S.amb = 1;
+      }
+      S.accept = acc;
     }
     team_sync<TW>(team);
     if (score_only) {
@@ -545,6 +567,7 @@ __global__ void __launch_bounds__(kWalkThreads, 4) walk_chain_kernel(WalkArgs A)
       A.final_score[c] = S.cur_total;
       A.accepted[c] = S.acc;
       A.tcount[c] = S.tcount;
+      if (A.ambiguous) A.ambiguous[c] = S.amb;
     }
   }
   if (lane == 0 && A.stat) {

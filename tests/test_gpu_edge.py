@@ -259,3 +259,30 @@ def test_walk_team_sizes_identical(tw):
         np.testing.assert_array_equal(rs[c].tracker_masks, o["tracker_masks"])
         np.testing.assert_array_equal(rs[c].final_order, o["final_order"])
         assert rs[c].accepted == o["accepted"]
+
+
+def test_device_acceptance_and_exact_replay():
+    """mh_accept on the device (CUDA log10) with ambiguity flags vs host glibc
+    thresholds: identical chains. A huge bound flags every chain, so every
+    chain is replayed with host thresholds, and results are still identical."""
+    import ctypes as C
+    data, pri, cfg, _ = P.baseline_instance("cfg3")
+    cache = P.ScoreCache.build(data, cfg, pri)
+    cfg.iterations, cfg.scan_mode = 150, 2
+    seeds = list(range(1, 41))
+    ref_b = None
+    for exact, tol in ((1, 0), (0, 0), (0, 30)):
+        cfg.exact_accept, cfg.accept_tol_log2 = exact, tol
+        b = P.run_chains_batch(cache, pri, seeds, cfg)
+        rep = C.c_uint64()
+        _lib.check(_lib.lib().bnmc_gpu_last_replayed(cache.handle, C.byref(rep)))
+        if tol == 30:
+            assert rep.value == len(seeds)
+        if ref_b is None:
+            ref_b = b
+            continue
+        for f in ("trace_proposed", "trace_accepted", "trace_best", "final_order", "final_score",
+                  "accepted", "tracker_count", "tracker_masks", "tracker_totals"):
+            np.testing.assert_array_equal(getattr(b, f), getattr(ref_b, f), err_msg=f)
+    o = port.run_mcmc(cache.table(), 4, 150, seeds[7], pri)
+    np.testing.assert_array_equal(ref_b.trace_proposed[7], o["trace_proposed"])
