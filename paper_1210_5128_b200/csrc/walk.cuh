@@ -90,10 +90,10 @@ __device__ __forceinline__ bool prefer_pos(uint64_t ma, uint64_t mb, int v, cons
 
 // global_index (combinatorics.cpp:61-76) with a shared-memory binomial table
 // bt[c * 9 + j] = C(c, j), j <= 8.
-__device__ __forceinline__ uint64_t gidx_smem(uint64_t mask, int c, int s, const uint64_t* bt) {
+__device__ __forceinline__ uint64_t gidx_smem(uint64_t mask, int c, const uint64_t* off,
+                                              const uint64_t* bt) {
   const int k = __popcll(mask);
-  uint64_t idx = 0;
-  for (int j = k + 1; j <= s; ++j) idx += bt[c * 9 + j];
+  uint64_t idx = off[k];  // sum_{j>k} C(c, j): the larger size classes come first
   int prev = 0, i = 0;
   for (uint64_t m = mask; m; m &= m - 1, ++i) {
     const int a = __ffsll((long long)m);
@@ -152,22 +152,68 @@ __device__ __forceinline__ bool walk_round(const double* re, const uint64_t* rc,
     e[u] = i < S ? __ldg(re + i) : -INFINITY;
     c[u] = i < S ? __ldg(rc + i) : ~0ull;
   }
+  // first group holding an admissible entry; its values selected without
+  // dynamic register indexing, then one set of shuffles
+  int hu = -1;
+  unsigned hb = 0;
 #pragma unroll
-  for (int u = 0; u < U; ++u) {
+  for (int u = U - 1; u >= 0; --u) {
     const unsigned bal = __ballot_sync(0xffffffffu, (c[u] & ncp) == 0);
-    if (bal && h.start == ~0ull) {
-      const int f = __ffs(bal) - 1;
-      h.start = base + u * 32 + f;
-      h.kstar = shfl_d(e[u], f);
-      h.kcm = shfl_u64(c[u], f);
-      // value of the next sorted entry, when it is in this round's registers
-      const bool known = f < 31 || u + 1 < U;
-      const double nx = f < 31 ? shfl_d(e[u], f + 1) : shfl_d(e[u + 1 < U ? u + 1 : u], 0);
-      h.next_differs = known && nx != h.kstar;
+    if (bal) {
+      hu = u;
+      hb = bal;
     }
   }
   base += 32 * U;
-  return h.start != ~0ull;
+  if (hu < 0) return false;
+  double eh = e[0], en = U > 1 ? e[1 < U ? 1 : 0] : e[0];
+  uint64_t ch = c[0];
+#pragma unroll
+  for (int u = 1; u < U; ++u)
+    if (u == hu) {
+      eh = e[u];
+      ch = c[u];
+      en = e[u + 1 < U ? u + 1 : u];
+    }
+  const int f = __ffs(hb) - 1;
+  h.start = base - 32 * U + hu * 32 + f;
+  h.kstar = shfl_d(eh, f);
+  h.kcm = shfl_u64(ch, f);
+  // value of the next sorted entry, when it is in this round's registers
+  const bool known = f < 31 || hu + 1 < U;
+  const double nx = shfl_d(f < 31 ? eh : en, (f + 1) & 31);
+  h.next_differs = known && nx != h.kstar;
+  return true;
+}
+
+// Admissible entries after sorted index `start` holding exactly kstar: the
+// reference keeps the first of them in predecessor-position order. Returns the
+// chosen candidate mask; *ties = number of further admissible equal entries.
+__device__ __noinline__ uint64_t collect_ties(const double* re, const uint64_t* rc, uint64_t ncp,
+                                              uint64_t S, uint64_t start, double kstar,
+                                              uint64_t kcm, int v, const uint8_t* ppos, int* ties_out) {
+  const int lane = threadIdx.x & 31;
+  uint64_t best_cm = kcm;
+  int ties = 0;
+  for (uint64_t i0 = start + 1;; i0 += 32) {
+    const uint64_t i = i0 + lane;
+    const bool eq = i < S && __ldg(re + i) == kstar;
+    const uint64_t cm = eq ? __ldg(rc + i) : ~0ull;
+    const bool adm = eq && (cm & ncp) == 0;
+    const unsigned bal = __ballot_sync(0xffffffffu, adm);
+    if (bal) {
+      ties += __popc(bal);
+      uint64_t mine = adm ? cm : ~0ull;
+      for (int o = 16; o > 0; o >>= 1) {
+        const uint64_t other = shfl_u64(mine, lane ^ o);
+        if (other != ~0ull && (mine == ~0ull || prefer_pos(other, mine, v, ppos))) mine = other;
+      }
+      if (prefer_pos(mine, best_cm, v, ppos)) best_cm = mine;
+    }
+    if (__ballot_sync(0xffffffffu, eq) != 0xffffffffu) break;
+  }
+  *ties_out = ties;
+  return best_cm;
 }
 
 struct PairOut {
@@ -180,7 +226,8 @@ struct PairOut {
 // predecessors are `cpred` (candidate positions). order[pos] = node, ppos[node]
 // = pos of the order being scored; bt = binomial table in shared memory.
 __device__ PairOut pair_argmax(const WalkArgs& A, int v, int p, uint64_t cpred, const uint8_t* order,
-                               const uint8_t* ppos, const uint64_t* bt, unsigned long long* walked,
+                               const uint8_t* ppos, const uint64_t* bt, const uint64_t* boff,
+                               unsigned long long* walked,
                                unsigned long long* enumerated) {
   const int lane = threadIdx.x & 31;
   PairOut r;
@@ -188,8 +235,7 @@ __device__ PairOut pair_argmax(const WalkArgs& A, int v, int p, uint64_t cpred, 
     // ---- enumeration in PST order (exact fp64, first maximum wins). Lane l
     // takes PST indices l, l+32, ...: ascending per lane, so strict '>' keeps
     // the first maximum; kEnumUnroll independent gathers are in flight.
-    uint32_t cnt = 0;
-    for (int j = 0; j <= A.s && j <= p; ++j) cnt += (uint32_t)bt[p * 9 + j];
+    const uint32_t off = A.pst_off[p], cnt = A.pst_off[p + 1] - off;
     double best = -INFINITY;
     uint32_t bj = 0xFFFFFFFFu;
     bool dup = false;
@@ -202,9 +248,9 @@ __device__ PairOut pair_argmax(const WalkArgs& A, int v, int p, uint64_t cpred, 
         nm[u] = 0;
         lv[u] = -INFINITY;
         if (j < cnt) {
-          const uint64_t pm = unrank_bt(j, p, A.s, bt);
+          const uint64_t pm = __ldg(A.pst + off + j);
           for (uint64_t m = pm; m; m &= m - 1) nm[u] |= 1ull << order[__ffsll((long long)m) - 1];
-          const uint64_t g = gidx_smem(nodes_to_cand(nm[u], v), A.n - 1, A.s, bt);
+          const uint64_t g = gidx_smem(nodes_to_cand(nm[u], v), A.n - 1, boff, bt);
           lv[u] = __ldg(A.ls + (uint64_t)v * A.S + g);
         }
       }
@@ -229,7 +275,7 @@ __device__ PairOut pair_argmax(const WalkArgs& A, int v, int p, uint64_t cpred, 
     const uint32_t jmin = __reduce_min_sync(0xffffffffu, at_max ? bj : 0xFFFFFFFFu);
     r.tied = __popc(win) > 1 || __any_sync(0xffffffffu, at_max && dup);
     r.eff = m;
-    const uint64_t pm = unrank_bt(jmin, p, A.s, bt);
+    const uint64_t pm = __ldg(A.pst + off + jmin);
     uint64_t nm = 0;
     for (uint64_t q = pm; q; q &= q - 1) nm |= 1ull << order[__ffsll((long long)q) - 1];
     r.cm = nodes_to_cand(nm, v);
@@ -269,28 +315,9 @@ __device__ PairOut pair_argmax(const WalkArgs& A, int v, int p, uint64_t cpred, 
   // Fast exit: the entry after `start` is still in registers of this round and
   // has a different value (exact ties are rare), so no tie is possible.
   if (next_differs) return r;
-  // Tie collection: admissible entries after `start` with eff == kstar.
-  uint64_t best_cm = kcm;
+  // Tie collection (rare): admissible entries after `start` with eff == kstar.
   int ties = 0;
-  for (uint64_t i0 = start + 1;; i0 += 32) {
-    const uint64_t i = i0 + lane;
-    const bool eq = i < S && __ldg(re + i) == kstar;
-    const uint64_t cm = eq ? __ldg(rc + i) : ~0ull;
-    const bool adm = eq && (cm & ncp) == 0;
-    const unsigned bal = __ballot_sync(0xffffffffu, adm);
-    if (bal) {
-      ties += __popc(bal);
-      // lane-local candidate, then a shuffle reduction under prefer_pos
-      uint64_t mine = adm ? cm : ~0ull;
-      for (int o = 16; o > 0; o >>= 1) {
-        const uint64_t other = shfl_u64(mine, lane ^ o);
-        if (other != ~0ull && (mine == ~0ull || prefer_pos(other, mine, v, ppos))) mine = other;
-      }
-      if (prefer_pos(mine, best_cm, v, ppos)) best_cm = mine;
-    }
-    if (__ballot_sync(0xffffffffu, eq) != 0xffffffffu) break;
-  }
-  r.cm = best_cm;
+  r.cm = collect_ties(re, rc, ncp, S, start, kstar, kcm, v, ppos, &ties);
   r.tied = ties > 0;
   return r;
 }
@@ -298,12 +325,11 @@ __device__ PairOut pair_argmax(const WalkArgs& A, int v, int p, uint64_t cpred, 
 // BestGraphTracker::update (sampler.cpp:32-41) by one warp: dedupe by full
 // graph equality, reject when full and total <= the minimum, insert at the
 // lower bound of (total desc, Dag operator< over the parent masks).
-__device__ void tracker_offer_warp(uint64_t* tm, double* tt, int K, int n, const uint64_t* pm,
-                                   double proposed, int* tcount) {
+__device__ __noinline__ void tracker_insert_warp(uint64_t* tm, double* tt, int K, int n,
+                                                 const uint64_t* pm, double proposed, int* tcount) {
   const int lane = threadIdx.x & 31;
   const int count = *tcount;
   const bool full = count == K;
-  if (full && proposed <= tt[count - 1]) return;
   for (int e = 0; e < count; ++e) {
     bool eq = true;
     for (int i = lane; i < n; i += 32) eq &= tm[(uint64_t)e * n + i] == pm[i];
@@ -343,6 +369,13 @@ __device__ void tracker_offer_warp(uint64_t* tm, double* tt, int K, int n, const
   __syncwarp();
 }
 
+__device__ __forceinline__ void tracker_offer_warp(uint64_t* tm, double* tt, int K, int n,
+                                                   const uint64_t* pm, double proposed, int* tcount) {
+  const int count = *tcount;
+  if (count == K && proposed <= tt[count - 1]) return;  // full: not above the minimum
+  tracker_insert_warp(tm, tt, K, n, pm, proposed, tcount);
+}
+
 // Barrier over the TW warps of one team (a team runs one chain).
 template <int TW>
 __device__ __forceinline__ void team_sync(int team) {
@@ -377,12 +410,18 @@ template <int TW>
 __global__ void __launch_bounds__(kWalkThreads, 4) walk_chain_kernel(WalkArgs A) {
   constexpr int kTeams = kWalkThreads / (32 * TW);
   __shared__ uint64_t s_bt[65 * 9];
+  __shared__ uint64_t s_boff[9];  // size-class offsets of global_index for c = n - 1
   __shared__ TeamState s_team[kTeams];
   const int tid = threadIdx.x, lane = tid & 31;
   const int team = (tid >> 5) / TW, twarp = (tid >> 5) % TW, ttid = tid - team * TW * 32;
   const int c = blockIdx.x * kTeams + team;
   const int n = A.n;
   for (int i = tid; i < 65 * 9; i += kWalkThreads) s_bt[i] = binom(i / 9, i % 9);
+  if (tid < 9) {
+    uint64_t o = 0;
+    for (int j = tid + 1; j <= A.s; ++j) o += binom(A.n - 1, j);
+    s_boff[tid] = o;
+  }
   __syncthreads();
   if (c >= A.C) return;  // whole teams only: no later CTA-wide barrier when TW < 8
   TeamState& S = s_team[team];
@@ -493,7 +532,8 @@ __global__ void __launch_bounds__(kWalkThreads, 4) walk_chain_kernel(WalkArgs A)
     // ---- exact argmax of every rescanned row, one warp per pair
     for (int q = twarp; q < np; q += TW) {
       const int v = S.pv[q];
-      const PairOut o = pair_argmax(A, v, S.pp[q], S.pc[q], S.prop, S.ppos, s_bt, &walked, &enumerated);
+      const PairOut o = pair_argmax(A, v, S.pp[q], S.pc[q], S.prop, S.ppos, s_bt, s_boff, &walked,
+                                    &enumerated);
       if (lane == 0) {
         S.pm[v] = cand_to_nodes(o.cm, v);
         S.pb[v] = o.eff;
