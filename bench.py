@@ -353,7 +353,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="cfg4")
-    ap.add_argument("--chains", type=int, default=4736, help="chains per GPU")
+    ap.add_argument("--chains", type=int, default=18944, help="chains per GPU (128 per SM)")
     ap.add_argument("--team-warps", type=int, default=0, help="warps per chain (0 auto)")
     ap.add_argument("--no-extras", action="store_true", help="skip single-chain/full-scan probes")
     ap.add_argument("--iters", type=int, default=500, help="MCMC iterations per chain per step")

@@ -163,6 +163,8 @@ struct bnmc_table {
   float sort_ms = 0.f;
   DevBuf<uint64_t> pst;
   DevBuf<uint32_t> pst_off;
+  DevBuf<uint64_t> pst2;
+  DevBuf<uint32_t> pst2_off;
   int pe = -1;
   int scan_mode = 0;  // default for score_orders: 0 auto (walk), 1 full-row scan
   DevBuf<int> d_fo, d_tc;
@@ -437,16 +439,14 @@ __global__ void eff64_kernel(const double* __restrict__ ls, const uint64_t* __re
 // PST of predecessor count p (enumerate_bounded_position_sets order,
 // combinatorics.hpp:83-101) for every p with S(p,s) <= kEnumMax: the walk
 // path enumerates those rows instead of walking them.
-void build_pst_small(bnmc_table* t) {
-  std::vector<uint64_t> masks;
-  std::vector<uint32_t> off(1, 0);
-  int pe = -1;
-  for (int p = 0; p < t->n; ++p) {
-    const uint64_t cnt = bounded_count(p, t->s);
-    if (cnt > kEnumMax) break;
+void build_pst_table(int n, int s, int pmax, std::vector<uint64_t>& masks, std::vector<uint32_t>& off) {
+  masks.clear();
+  off.assign(1, 0);
+  for (int p = 0; p <= pmax; ++p) {
+    const uint64_t cnt = s < 0 ? 0 : bounded_count(p, s);
     for (uint64_t j = 0; j < cnt; ++j) {
       uint64_t r = j;
-      int k = std::min(t->s, p);
+      int k = std::min(s, p);
       for (; k >= 0; --k) {
         const uint64_t block = hbinom(p, k);
         if (r < block) break;
@@ -460,14 +460,30 @@ void build_pst_small(bnmc_table* t) {
       masks.push_back(m);
     }
     off.push_back(static_cast<uint32_t>(masks.size()));
-    pe = p;
   }
+  (void)n;
+}
+
+// PST of predecessor count p (enumerate_bounded_position_sets order,
+// combinatorics.hpp:83-101) for every p with S(p,s) <= kEnumMax: the walk
+// path enumerates those rows instead of walking them; plus PST(p, s-1) for
+// p < pe (the sets containing one given position, for delta rescans).
+void build_pst_small(bnmc_table* t) {
+  int pe = -1;
+  for (int p = 0; p < t->n && bounded_count(p, t->s) <= kEnumMax; ++p) pe = p;
   t->pe = pe;
-  t->pst.alloc(std::max<size_t>(masks.size(), 1));
-  t->pst_off.alloc(off.size());
-  if (!masks.empty())
-    CK(cudaMemcpyAsync(t->pst.p, masks.data(), masks.size() * 8, cudaMemcpyHostToDevice, t->stream));
-  CK(cudaMemcpyAsync(t->pst_off.p, off.data(), off.size() * 4, cudaMemcpyHostToDevice, t->stream));
+  std::vector<uint64_t> m1, m2;
+  std::vector<uint32_t> o1, o2;
+  build_pst_table(t->n, t->s, pe, m1, o1);
+  build_pst_table(t->n, t->s - 1, std::max(pe - 1, 0), m2, o2);
+  t->pst.alloc(std::max<size_t>(m1.size(), 1));
+  t->pst_off.alloc(o1.size());
+  t->pst2.alloc(std::max<size_t>(m2.size(), 1));
+  t->pst2_off.alloc(o2.size());
+  if (!m1.empty()) CK(cudaMemcpyAsync(t->pst.p, m1.data(), m1.size() * 8, cudaMemcpyHostToDevice, t->stream));
+  CK(cudaMemcpyAsync(t->pst_off.p, o1.data(), o1.size() * 4, cudaMemcpyHostToDevice, t->stream));
+  if (!m2.empty()) CK(cudaMemcpyAsync(t->pst2.p, m2.data(), m2.size() * 8, cudaMemcpyHostToDevice, t->stream));
+  CK(cudaMemcpyAsync(t->pst2_off.p, o2.data(), o2.size() * 4, cudaMemcpyHostToDevice, t->stream));
   CK(cudaStreamSynchronize(t->stream));  // host vectors die here
 }
 
@@ -539,6 +555,8 @@ WalkArgs walk_args(bnmc_table* t) {
   A.w = t->w.p;
   A.pst = t->pst.p;
   A.pst_off = t->pst_off.p;
+  A.pst2 = t->pst2.p;
+  A.pst2_off = t->pst2_off.p;
   A.pe = t->pe;
   A.S = t->S;
   A.n = t->n;

@@ -34,8 +34,18 @@ namespace bnmc_dev {
 
 constexpr int kWalkThreads = 256;
 constexpr int kWalkWarps = kWalkThreads / 32;
-constexpr int kWalkUnroll = 8;             // entries per lane per walk round
-constexpr int kEnumUnroll = 4;             // independent gathers per lane per enumeration step
+#ifndef BNMC_WALK_UNROLL
+#define BNMC_WALK_UNROLL 4
+#endif
+constexpr int kWalkUnroll = BNMC_WALK_UNROLL;  // entries per lane per (deep) walk round
+#ifndef BNMC_WALK_MINB1
+#define BNMC_WALK_MINB1 4
+#endif
+constexpr int kWalkMinBlocks1 = BNMC_WALK_MINB1;  // CTAs per SM targeted for one-warp chains
+#ifndef BNMC_ENUM_UNROLL
+#define BNMC_ENUM_UNROLL 1
+#endif
+constexpr int kEnumUnroll = BNMC_ENUM_UNROLL;  // independent gathers per lane per enumeration step
 constexpr uint64_t kEnumMax = 1024;        // enumerate when S(p,s) <= this
 
 struct WalkArgs {
@@ -45,6 +55,8 @@ struct WalkArgs {
   const double* __restrict__ w;       // [n][n] PPF weights
   const uint64_t* __restrict__ pst;   // position masks of PST(p) for p <= pe, concatenated
   const uint32_t* __restrict__ pst_off;  // [pe+2]
+  const uint64_t* __restrict__ pst2;  // PST(p, s-1) for p < pe: sets of the other positions
+  const uint32_t* __restrict__ pst2_off;  // [pe+1]
   int pe;                              // largest enumerated predecessor count
   uint64_t S;
   int n, s;
@@ -225,61 +237,104 @@ struct PairOut {
 // Warp-cooperative exact argmax of row v for the node at position p whose
 // predecessors are `cpred` (candidate positions). order[pos] = node, ppos[node]
 // = pos of the order being scored; bt = binomial table in shared memory.
+// Exact argmax over the position subsets listed in pst[0..cnt) (PST order:
+// first maximum wins, as scan_slice + argmax_reduce). ins >= 0 inserts that
+// position into every listed subset (the listed subsets then range over the
+// other positions): used to enumerate only the sets containing one node.
+__device__ __forceinline__ PairOut enum_pst(const WalkArgs& A, int v, const uint64_t* __restrict__ pst, uint32_t cnt,
+                            int ins, const uint8_t* order, const uint64_t* bt, const uint64_t* boff) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t lowm = ins >= 0 ? (1ull << ins) - 1 : ~0ull;
+  const uint64_t insb = ins >= 0 ? 1ull << ins : 0ull;
+  double best = -INFINITY;
+  uint32_t bj = 0xFFFFFFFFu;
+  bool dup = false;
+  for (uint32_t j0 = 0; j0 < cnt; j0 += 32 * kEnumUnroll) {
+    uint64_t nm[kEnumUnroll];
+    double lv[kEnumUnroll];
+#pragma unroll
+    for (int u = 0; u < kEnumUnroll; ++u) {
+      const uint32_t j = j0 + u * 32 + lane;
+      nm[u] = 0;
+      lv[u] = -INFINITY;
+      if (j < cnt) {
+        const uint64_t pm0 = __ldg(pst + j);
+        const uint64_t pm = (pm0 & lowm) | ((pm0 & ~lowm) << 1) | insb;
+        for (uint64_t m = pm; m; m &= m - 1) nm[u] |= 1ull << order[__ffsll((long long)m) - 1];
+        const uint64_t g = gidx_smem(nodes_to_cand(nm[u], v), A.n - 1, boff, bt);
+        lv[u] = __ldg(A.ls + (uint64_t)v * A.S + g);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kEnumUnroll; ++u) {
+      const uint32_t j = j0 + u * 32 + lane;
+      if (j >= cnt) continue;
+      const double e = lv[u] + ppf_sum(A.w, A.n, v, nm[u]);
+      if (e > best) {
+        best = e;
+        bj = j;
+        dup = false;
+      } else if (e == best) {
+        dup = true;
+      }
+    }
+  }
+  double m = best;
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  const bool at_max = best == m && bj != 0xFFFFFFFFu;
+  const unsigned win = __ballot_sync(0xffffffffu, at_max);
+  const uint32_t jmin = __reduce_min_sync(0xffffffffu, at_max ? bj : 0xFFFFFFFFu);
+  PairOut r;
+  r.tied = __popc(win) > 1 || __any_sync(0xffffffffu, at_max && dup);
+  r.eff = m;
+  r.cm = 0;
+  if (jmin != 0xFFFFFFFFu) {
+    const uint64_t pm0 = __ldg(pst + jmin);
+    const uint64_t pm = (pm0 & lowm) | ((pm0 & ~lowm) << 1) | insb;
+    uint64_t nm = 0;
+    for (uint64_t q = pm; q; q &= q - 1) nm |= 1ull << order[__ffsll((long long)q) - 1];
+    r.cm = nodes_to_cand(nm, v);
+  }
+  return r;
+}
+
+// Row of a node whose predecessor set changed from P to P - {X} + {Y}, whose
+// current best (old_eff, old_cm) does not contain X and is not an exact tie:
+// the best over P' is the better of the old best and the best set containing
+// Y (any other admissible set was admissible before and scored <= old_eff).
+struct DeltaIn {
+  bool on;
+  int ypos;        // position of Y in the proposed order
+  double old_eff;
+  uint64_t old_cm;  // candidate mask of the current best
+};
+
+// Warp-cooperative exact argmax of row v for the node at position p whose
+// predecessors are `cpred` (candidate positions). order[pos] = node, ppos[node]
+// = pos of the order being scored; bt = binomial table in shared memory.
 __device__ PairOut pair_argmax(const WalkArgs& A, int v, int p, uint64_t cpred, const uint8_t* order,
                                const uint8_t* ppos, const uint64_t* bt, const uint64_t* boff,
-                               unsigned long long* walked,
+                               const DeltaIn& d, unsigned long long* walked,
                                unsigned long long* enumerated) {
   const int lane = threadIdx.x & 31;
   PairOut r;
   if (p <= A.pe) {
-    // ---- enumeration in PST order (exact fp64, first maximum wins). Lane l
-    // takes PST indices l, l+32, ...: ascending per lane, so strict '>' keeps
-    // the first maximum; kEnumUnroll independent gathers are in flight.
-    const uint32_t off = A.pst_off[p], cnt = A.pst_off[p + 1] - off;
-    double best = -INFINITY;
-    uint32_t bj = 0xFFFFFFFFu;
-    bool dup = false;
-    for (uint32_t j0 = 0; j0 < cnt; j0 += 32 * kEnumUnroll) {
-      uint64_t nm[kEnumUnroll];
-      double lv[kEnumUnroll];
-#pragma unroll
-      for (int u = 0; u < kEnumUnroll; ++u) {
-        const uint32_t j = j0 + u * 32 + lane;
-        nm[u] = 0;
-        lv[u] = -INFINITY;
-        if (j < cnt) {
-          const uint64_t pm = __ldg(A.pst + off + j);
-          for (uint64_t m = pm; m; m &= m - 1) nm[u] |= 1ull << order[__ffsll((long long)m) - 1];
-          const uint64_t g = gidx_smem(nodes_to_cand(nm[u], v), A.n - 1, boff, bt);
-          lv[u] = __ldg(A.ls + (uint64_t)v * A.S + g);
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < kEnumUnroll; ++u) {
-        const uint32_t j = j0 + u * 32 + lane;
-        if (j >= cnt) continue;
-        const double e = lv[u] + ppf_sum(A.w, A.n, v, nm[u]);
-        if (e > best) {
-          best = e;
-          bj = j;
-          dup = false;
-        } else if (e == best) {
-          dup = true;
-        }
+    // delta rows: the sets containing Y only (PST(p-1, s-1) with Y's position
+    // inserted); otherwise every admissible set (PST(p, s))
+    const uint64_t* pst = d.on ? A.pst2 + A.pst2_off[p - 1] : A.pst + A.pst_off[p];
+    const uint32_t cnt = d.on ? A.pst2_off[p] - A.pst2_off[p - 1] : A.pst_off[p + 1] - A.pst_off[p];
+    r = enum_pst(A, v, pst, cnt, d.on ? d.ypos : -1, order, bt, boff);
+    if (lane == 0) *enumerated += cnt;
+    if (d.on) {
+      if (!(r.eff >= d.old_eff)) {  // also covers cnt == 0 (s == 0)
+        r.eff = d.old_eff;
+        r.cm = d.old_cm;
+        r.tied = 0;
+      } else if (r.eff == d.old_eff) {
+        r.tied = 1;
+        if (prefer_pos(d.old_cm, r.cm, v, ppos)) r.cm = d.old_cm;
       }
     }
-    double m = best;
-    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-    const bool at_max = best == m && bj != 0xFFFFFFFFu;
-    const unsigned win = __ballot_sync(0xffffffffu, at_max);
-    const uint32_t jmin = __reduce_min_sync(0xffffffffu, at_max ? bj : 0xFFFFFFFFu);
-    r.tied = __popc(win) > 1 || __any_sync(0xffffffffu, at_max && dup);
-    r.eff = m;
-    const uint64_t pm = __ldg(A.pst + off + jmin);
-    uint64_t nm = 0;
-    for (uint64_t q = pm; q; q &= q - 1) nm |= 1ull << order[__ffsll((long long)q) - 1];
-    r.cm = nodes_to_cand(nm, v);
-    if (lane == 0) *enumerated += cnt;
     return r;
   }
   // ---- walk of the sorted row
@@ -392,6 +447,7 @@ __device__ __forceinline__ void team_sync(int team) {
 struct TeamState {
   uint8_t order[64], prop[64], ppos[64];
   uint8_t pv[64], pp[64], pt[64];  // pair -> node, position, exact-tie flag
+  uint8_t pd[64];                  // pair -> delta rescan eligible (P' = P - X + Y)
   uint64_t pc[64];                 // pair -> candidate predecessor mask
   uint64_t pm[64];                 // proposed graph (parent node masks by node)
   double pb[64];                   // proposed per-node bests
@@ -407,16 +463,18 @@ struct TeamState {
 // chain the whole CTA (lowest latency per iteration); TW = 1 runs a chain per
 // warp, barrier-free, for throughput over many chains.
 template <int TW>
-__global__ void __launch_bounds__(kWalkThreads, 4) walk_chain_kernel(WalkArgs A) {
+__global__ void __launch_bounds__(kWalkThreads, TW == 1 ? kWalkMinBlocks1 : 4) walk_chain_kernel(WalkArgs A) {
   constexpr int kTeams = kWalkThreads / (32 * TW);
   __shared__ uint64_t s_bt[65 * 9];
   __shared__ uint64_t s_boff[9];  // size-class offsets of global_index for c = n - 1
+  __shared__ unsigned long long s_stat[kWalkWarps][2];  // per warp: walked, enumerated
   __shared__ TeamState s_team[kTeams];
   const int tid = threadIdx.x, lane = tid & 31;
   const int team = (tid >> 5) / TW, twarp = (tid >> 5) % TW, ttid = tid - team * TW * 32;
   const int c = blockIdx.x * kTeams + team;
   const int n = A.n;
   for (int i = tid; i < 65 * 9; i += kWalkThreads) s_bt[i] = binom(i / 9, i % 9);
+  if (tid < 2 * kWalkWarps) (&s_stat[0][0])[tid] = 0;
   if (tid < 9) {
     uint64_t o = 0;
     for (int j = tid + 1; j <= A.s; ++j) o += binom(A.n - 1, j);
@@ -452,7 +510,9 @@ __global__ void __launch_bounds__(kWalkThreads, 4) walk_chain_kernel(WalkArgs A)
     S.cur_total = 0.0;
   }
   team_sync<TW>(team);
-  unsigned long long walked = 0, enumerated = 0, pairs = 0;
+  unsigned long long* walked = &s_stat[tid >> 5][0];
+  unsigned long long* enumerated = &s_stat[tid >> 5][1];
+  unsigned long long pairs = 0;
   double thr_t = 0.0;
   const uint64_t T = score_only ? 0 : A.iters;
   for (uint64_t t = 0; t <= T; ++t) {
@@ -523,6 +583,11 @@ __global__ void __launch_bounds__(kWalkThreads, 4) walk_chain_kernel(WalkArgs A)
         S.pv[slot] = (uint8_t)v;
         S.pp[slot] = (uint8_t)p;
         S.pc[slot] = nodes_to_cand(pre[h], v);
+        // middle rows of a swap: the node at hi (X) left the predecessors, the
+        // node at lo (Y) joined; eligible when the current best avoids X and
+        // is not an exact tie
+        S.pd[slot] = (uint8_t)(t > 0 && p > lo && p < hi && p <= A.pe &&
+                               !((S.tied >> v) & 1ull) && !((S.cm[v] >> S.prop[hi]) & 1ull));
         ++slot;
       }
       if (lane == 31) S.np = cnt;
@@ -532,8 +597,13 @@ __global__ void __launch_bounds__(kWalkThreads, 4) walk_chain_kernel(WalkArgs A)
     // ---- exact argmax of every rescanned row, one warp per pair
     for (int q = twarp; q < np; q += TW) {
       const int v = S.pv[q];
-      const PairOut o = pair_argmax(A, v, S.pp[q], S.pc[q], S.prop, S.ppos, s_bt, s_boff, &walked,
-                                    &enumerated);
+      DeltaIn d;
+      d.on = S.pd[q] != 0;
+      d.ypos = lo;
+      d.old_eff = S.cb[v];
+      d.old_cm = nodes_to_cand(S.cm[v], v);
+      const PairOut o = pair_argmax(A, v, S.pp[q], S.pc[q], S.prop, S.ppos, s_bt, s_boff, d,
+                                    walked, enumerated);
       if (lane == 0) {
         S.pm[v] = cand_to_nodes(o.cm, v);
         S.pb[v] = o.eff;
@@ -611,8 +681,8 @@ __global__ void __launch_bounds__(kWalkThreads, 4) walk_chain_kernel(WalkArgs A)
     }
   }
   if (lane == 0 && A.stat) {
-    atomicAdd(A.stat + 1, walked);
-    atomicAdd(A.stat + 2, enumerated);
+    atomicAdd(A.stat + 1, *walked);
+    atomicAdd(A.stat + 2, *enumerated);
     if (twarp == 0) atomicAdd(A.stat, pairs);
   }
 }
