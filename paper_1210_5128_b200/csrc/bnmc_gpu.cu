@@ -159,6 +159,8 @@ struct bnmc_table {
   // lazily after the priors are folded; PST of small predecessor counts.
   DevBuf<double> seff;
   DevBuf<uint64_t> scm;
+  DevBuf<double> eff;  // eff = ls + PpfTable::sum in global-index order
+  uint64_t Sw = 0;     // sorted row stride
   bool sorted_valid = false;
   float sort_ms = 0.f;
   DevBuf<uint64_t> pst;
@@ -424,6 +426,15 @@ TieCtx tie_ctx(const bnmc_table* t) {
 
 // eff = ls + PpfTable::sum in the scan's association (engine.cpp:50-51), fp64,
 // with each entry's candidate mask: the input of the per-row sort.
+// Padding of the sorted rows: eff -inf, mask ~0 (never admissible).
+__global__ void pad_sorted_kernel(double* seff, uint64_t* scm, uint64_t S, uint64_t Sw) {
+  const uint64_t v = blockIdx.y;
+  for (uint64_t i = S + threadIdx.x; i < Sw; i += blockDim.x) {
+    seff[v * Sw + i] = -INFINITY;
+    scm[v * Sw + i] = ~0ull;
+  }
+}
+
 __global__ void eff64_kernel(const double* __restrict__ ls, const uint64_t* __restrict__ cmask,
                              const double* __restrict__ w, double* eff, uint64_t* cm, int n,
                              uint64_t S) {
@@ -493,29 +504,34 @@ void ensure_sorted(bnmc_table* t) {
   if (t->sorted_valid) return;
   if (t->pe < 0 && t->pst_off.n == 0) build_pst_small(t);
   const uint64_t N = static_cast<uint64_t>(t->n) * t->S;
-  t->seff.alloc(N);
-  t->scm.alloc(N);
-  DevBuf<double> keys;
+  // sorted rows padded with never-admissible entries so walk rounds need no
+  // bounds checks: row stride Sw >= S + one full round
+  t->Sw = (t->S + 32 * kWalkUnroll + 31) / 32 * 32;
+  const uint64_t NW = static_cast<uint64_t>(t->n) * t->Sw;
+  t->seff.alloc(NW);
+  t->scm.alloc(NW);
+  t->eff.alloc(N);  // eff in global-index order (kept: the enumeration gathers it)
   DevBuf<uint64_t> vals;
-  keys.alloc(N);
   vals.alloc(N);
   cudaEvent_t e0, e1;
   CK(cudaEventCreate(&e0));
   CK(cudaEventCreate(&e1));
   CK(cudaEventRecord(e0, t->stream));
   const unsigned bx = static_cast<unsigned>(std::min<uint64_t>((t->S + 255) / 256, 4096));
-  eff64_kernel<<<dim3(bx, t->n), 256, 0, t->stream>>>(t->ls.p, t->cmask.p, t->w.p, keys.p, vals.p,
+  eff64_kernel<<<dim3(bx, t->n), 256, 0, t->stream>>>(t->ls.p, t->cmask.p, t->w.p, t->eff.p, vals.p,
                                                         t->n, t->S);
   CK(cudaGetLastError());
+  pad_sorted_kernel<<<dim3(1, t->n), 256, 0, t->stream>>>(t->seff.p, t->scm.p, t->S, t->Sw);
+  CK(cudaGetLastError());
   size_t temp_bytes = 0;
-  CK(cub::DeviceRadixSort::SortPairsDescending(nullptr, temp_bytes, keys.p, t->seff.p, vals.p,
+  CK(cub::DeviceRadixSort::SortPairsDescending(nullptr, temp_bytes, t->eff.p, t->seff.p, vals.p,
                                                t->scm.p, static_cast<int>(t->S), 0, 64, t->stream));
   DevBuf<uint8_t> temp;
   temp.alloc(std::max<size_t>(temp_bytes, 1));
   for (int v = 0; v < t->n; ++v) {
-    const uint64_t o = static_cast<uint64_t>(v) * t->S;
-    CK(cub::DeviceRadixSort::SortPairsDescending(temp.p, temp_bytes, keys.p + o, t->seff.p + o,
-                                                 vals.p + o, t->scm.p + o, static_cast<int>(t->S),
+    const uint64_t o = static_cast<uint64_t>(v) * t->S, ow = static_cast<uint64_t>(v) * t->Sw;
+    CK(cub::DeviceRadixSort::SortPairsDescending(temp.p, temp_bytes, t->eff.p + o, t->seff.p + ow,
+                                                 vals.p + o, t->scm.p + ow, static_cast<int>(t->S),
                                                  0, 64, t->stream));
   }
   CK(cudaEventRecord(e1, t->stream));
@@ -551,6 +567,8 @@ WalkArgs walk_args(bnmc_table* t) {
   WalkArgs A{};
   A.seff = t->seff.p;
   A.scm = t->scm.p;
+  A.eff = t->eff.p;
+  A.Sw = t->Sw;
   A.ls = t->ls.p;
   A.w = t->w.p;
   A.pst = t->pst.p;

@@ -49,8 +49,10 @@ constexpr int kEnumUnroll = BNMC_ENUM_UNROLL;  // independent gathers per lane p
 constexpr uint64_t kEnumMax = 1024;        // enumerate when S(p,s) <= this
 
 struct WalkArgs {
-  const double* __restrict__ seff;    // [n][S] eff, sorted descending per row
-  const uint64_t* __restrict__ scm;   // [n][S] candidate masks in the same order
+  const double* __restrict__ seff;    // [n][Sw] eff, sorted descending per row, padded
+  const uint64_t* __restrict__ scm;   // [n][Sw] candidate masks in the same order
+  const double* __restrict__ eff;     // [n][S] eff in global-index order
+  uint64_t Sw;                        // sorted row stride (>= S + one walk round)
   const double* __restrict__ ls;      // [n][S] local scores, BNSC order
   const double* __restrict__ w;       // [n][n] PPF weights
   const uint64_t* __restrict__ pst;   // position masks of PST(p) for p <= pe, concatenated
@@ -160,9 +162,9 @@ __device__ __forceinline__ bool walk_round(const double* re, const uint64_t* rc,
   uint64_t c[U];
 #pragma unroll
   for (int u = 0; u < U; ++u) {
-    const uint64_t i = base + u * 32 + lane;
-    e[u] = i < S ? __ldg(re + i) : -INFINITY;
-    c[u] = i < S ? __ldg(rc + i) : ~0ull;
+    const uint64_t i = base + u * 32 + lane;  // < Sw: rows are padded by one round
+    e[u] = __ldg(re + i);
+    c[u] = __ldg(rc + i);
   }
   // first group holding an admissible entry; its values selected without
   // dynamic register indexing, then one set of shuffles
@@ -262,14 +264,14 @@ __device__ __forceinline__ PairOut enum_pst(const WalkArgs& A, int v, const uint
         const uint64_t pm = (pm0 & lowm) | ((pm0 & ~lowm) << 1) | insb;
         for (uint64_t m = pm; m; m &= m - 1) nm[u] |= 1ull << order[__ffsll((long long)m) - 1];
         const uint64_t g = gidx_smem(nodes_to_cand(nm[u], v), A.n - 1, boff, bt);
-        lv[u] = __ldg(A.ls + (uint64_t)v * A.S + g);
+        lv[u] = __ldg(A.eff + (uint64_t)v * A.S + g);
       }
     }
 #pragma unroll
     for (int u = 0; u < kEnumUnroll; ++u) {
       const uint32_t j = j0 + u * 32 + lane;
       if (j >= cnt) continue;
-      const double e = lv[u] + ppf_sum(A.w, A.n, v, nm[u]);
+      const double e = lv[u];  // ls + PpfTable::sum, precomputed (eff64_kernel)
       if (e > best) {
         best = e;
         bj = j;
@@ -338,8 +340,8 @@ __device__ PairOut pair_argmax(const WalkArgs& A, int v, int p, uint64_t cpred, 
     return r;
   }
   // ---- walk of the sorted row
-  const double* re = A.seff + (uint64_t)v * A.S;
-  const uint64_t* rc = A.scm + (uint64_t)v * A.S;
+  const double* re = A.seff + (uint64_t)v * A.Sw;
+  const uint64_t* rc = A.scm + (uint64_t)v * A.Sw;
   const uint64_t ncp = ~cpred;
   const uint64_t S = A.S;
   WalkHit h;
