@@ -217,11 +217,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     tot_dev = sum(dev_ms) / 1e3
     tot_wall = sum(wall_s)
-    recs = np.zeros((Cn, 3 + data.n), np.float64)
-    recs[:, 0] = D.chain_seeds(1, rank, Cn, args.steps - 1, world).astype(np.float64)
-    recs[:, 1] = out.accepted.astype(np.float64)
-    recs[:, 2] = out.tracker_totals[:, 0]
-    recs[:, 3:] = out.tracker_masks[:, 0, :].view(np.float64)
+    recs = D.chain_records_from_batch(out, D.chain_seeds(1, rank, Cn, args.steps - 1, world), n)
     if world > 1:
         import torch.distributed as tdist
         tt = torch.tensor([tot_dev, tot_wall, pre_s], device="cuda", dtype=torch.float64)
@@ -241,7 +237,7 @@ def run_ours(args):
     peak, peak_src = load_peaks()
     out_line = None
     if rank == 0:
-        best_i = int(np.argmax(allrec[:, 2]))
+        best = D.best_overall(allrec, n)
         cpu = None
         extra = {}
         if world == 1 and not args.no_cpu_baseline:
@@ -287,7 +283,7 @@ def run_ours(args):
                      "chains_replayed_exact": replayed},
             "precompute_s": pre_s, "precompute_kernel_ms": k1.value, "fold_ms": fold.value,
             "gpu_launches": int(args.steps * (1 + (1 if replayed else 0))),
-            "best_total": float(allrec[best_i, 2]),
+            "best_total": best["best_total"], "best_chain_seed": best["seed"],
             "cpu_baseline": cpu,
             "clocks": clocks.summary(),
         }

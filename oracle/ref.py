@@ -96,6 +96,13 @@ def lib():
                                _f64p, _u8p, _f64p, _i32p, C.POINTER(C.c_double),
                                C.POINTER(C.c_uint64), C.POINTER(C.c_int), _u64p, _f64p,
                                C.POINTER(C.c_double), C.POINTER(C.c_double)]
+    L.ref_write_dataset_csv.argtypes = [_u8p, _i32p, C.c_int, C.c_uint64, C.c_char_p]
+    L.ref_write_prior_csv.argtypes = [_f64p, C.c_int, C.c_char_p]
+    L.ref_write_edge_list.argtypes = [_u64p, C.c_int, C.c_char_p]
+    L.ref_learn.argtypes = [C.c_char_p, C.c_char_p, C.c_int, C.c_double, C.c_double, C.c_int,
+                            C.c_uint64, C.c_uint64, C.c_int, C.c_int, C.c_int, C.c_char_p]
+    L.ref_eval_sweep.argtypes = [C.c_char_p, C.c_char_p, C.c_int, C.c_double, C.c_double,
+                                 C.c_uint64, C.c_uint64, C.c_int, C.c_int, C.c_char_p]
     _lib = L
     return L
 
@@ -320,3 +327,38 @@ def run_mcmc(cells, cards, s, iterations, seed, priors=None, gamma=0.1, ess=1.0,
 
 def max_threads():
     return lib().ref_max_threads()
+
+
+def write_dataset_csv(cells, cards, path):
+    """The reference's write_dataset_csv (io.cpp:128-141)."""
+    cells = np.ascontiguousarray(cells, np.uint8)
+    m, n = cells.shape
+    _check(lib().ref_write_dataset_csv(cells.ravel(), np.ascontiguousarray(cards, np.int32), n, m,
+                                       str(path).encode()))
+
+
+def write_prior_csv(r, path):
+    r = np.ascontiguousarray(r, np.float64)
+    _check(lib().ref_write_prior_csv(r.ravel(), r.shape[0], str(path).encode()))
+
+
+def write_edge_list(masks, path):
+    masks = np.ascontiguousarray(masks, np.uint64)
+    _check(lib().ref_write_edge_list(masks, masks.size, str(path).encode()))
+
+
+def learn(data_path, out_prefix, s=4, iterations=1, seed=0, priors_path=None, gamma=0.1, ess=1.0,
+          k2=False, workers=None, track_top=10, strict=False):
+    """The reference CLI's `learn` (bnmc.cpp:100-138) through its own library."""
+    _check(lib().ref_learn(str(data_path).encode(),
+                           None if priors_path is None else str(priors_path).encode(), s, gamma,
+                           ess, int(k2), iterations, seed, workers or max_threads(), track_top,
+                           int(strict), str(out_prefix).encode()))
+
+
+def eval_sweep(truth_path, data_path, out_path, s=4, iterations=1, seed=0, gamma=0.1, ess=1.0,
+               workers=None, track_top=10):
+    """The reference CLI's `eval --sweep` (bnmc.cpp:160-212)."""
+    _check(lib().ref_eval_sweep(str(truth_path).encode(), str(data_path).encode(), s, gamma, ess,
+                                iterations, seed, workers or max_threads(), track_top,
+                                str(out_path).encode()))

@@ -15,6 +15,7 @@
 #include <cstdint>
 #include <cstring>
 #include <exception>
+#include <fstream>
 #include <numeric>
 #include <string>
 #include <vector>
@@ -22,6 +23,7 @@
 #include "bnmc/combinatorics.hpp"
 #include "bnmc/engine.hpp"
 #include "bnmc/evalgen.hpp"
+#include "bnmc/io.hpp"
 #include "bnmc/rng.hpp"
 #include "bnmc/sampler.hpp"
 #include "bnmc/scoring.hpp"
@@ -344,6 +346,88 @@ int ref_run_mcmc(const std::uint8_t* cells, const int* cards, int n,
     }
     *preprocess_s = r.preprocess_seconds;
     *sampling_s = r.sampling_seconds;
+  });
+}
+
+// ---- L6 driver steps (tools/bnmc.cpp), restated with the reference's own io.cpp
+// writers so CLI outputs of the B200 build can be compared byte for byte.
+int ref_write_dataset_csv(const std::uint8_t* cells, const int* cards, int n, std::uint64_t m,
+                          const char* path) {
+  return guarded([&] { write_dataset_csv(path, make_dataset(cells, cards, n, m)); });
+}
+
+int ref_write_prior_csv(const double* r, int n, const char* path) {
+  return guarded([&] { write_prior_csv(path, make_priors(r, n)); });
+}
+
+int ref_write_edge_list(const std::uint64_t* masks, int n, const char* path) {
+  return guarded([&] {
+    std::vector<ParentSet> ps(n);
+    for (int i = 0; i < n; ++i) ps[i] = ParentSet{masks[i]};
+    write_edge_list(path, Dag(ps));
+  });
+}
+
+// run_learn (bnmc.cpp:100-138) without --save/--load-cache.
+int ref_learn(const char* data_path, const char* priors_path, int s, double gamma, double ess,
+              int k2, std::uint64_t iterations, std::uint64_t seed, int workers, int track_top,
+              int strict, const char* out_prefix) {
+  return guarded([&] {
+    RunConfig cfg = make_cfg(s, gamma, ess, k2, workers, std::uint64_t{4} << 30);
+    cfg.iterations = iterations;
+    cfg.seed = seed;
+    cfg.track_top = track_top;
+    cfg.strict_paper_tracker = strict != 0;
+    cfg.validate();
+    const Dataset data = read_dataset_csv(data_path);
+    if (data.rows() == 0) throw DataError(std::string(data_path) + ": no data rows");
+    const PriorMatrix priors = priors_path ? read_prior_csv(priors_path, data.n())
+                                           : PriorMatrix::neutral(data.n());
+    const McmcResult result = run_mcmc(data, cfg, priors, nullptr);
+    const std::string p = out_prefix;
+    write_summary(p + ".summary.txt", cfg, result);
+    write_trace_csv(p + ".trace.csv", result.trace);
+    write_edge_list(p + ".best.edges", result.tracker.best().dag);
+  });
+}
+
+// run_eval --sweep (bnmc.cpp:160-212), metrics CSV to out_path.
+int ref_eval_sweep(const char* truth_path, const char* data_path, int s, double gamma,
+                   double ess, std::uint64_t iterations, std::uint64_t seed, int workers,
+                   int track_top, const char* out_path) {
+  return guarded([&] {
+    std::ofstream out(out_path);
+    auto row = [&](const std::string& label, double hi, double lo, double fraction,
+                   const ConfusionCounts& c, double best) {
+      out << label << "," << format_double(hi) << "," << format_double(lo) << ","
+          << format_double(fraction) << "," << c.tp << "," << c.fp << "," << c.fn << "," << c.tn
+          << "," << format_double(c.tp_rate()) << "," << format_double(c.fp_rate()) << ","
+          << format_double(c.f1()) << "," << format_double(best) << "\n";
+    };
+    out << "label,prior_hi,prior_lo,fraction,tp,fp,fn,tn,tp_rate,fp_rate,f1,best_score\n";
+    const Dag truth = read_edge_list(truth_path, 0);
+    const Dataset data = read_dataset_csv(data_path);
+    RunConfig cfg = make_cfg(s, gamma, ess, 0, workers, std::uint64_t{4} << 30);
+    cfg.iterations = iterations;
+    cfg.seed = seed;
+    cfg.track_top = track_top;
+    cfg.validate();
+    const ScoreCache cache = ScoreCache::build(data, cfg);
+    const McmcResult base = run_mcmc(data, cfg, PriorMatrix::neutral(data.n()), &cache);
+    const Dag& bd = base.tracker.best().dag;
+    row("baseline", 0.5, 0.5, 0.0, confusion(bd, truth), base.tracker.best_score());
+    const std::pair<double, double> pairs[2] = {{0.7, 0.2}, {0.8, 0.1}};
+    const double fractions[2] = {0.2, 0.4};
+    const Rng master(cfg.seed);
+    int k = 0;
+    for (const auto& pr : pairs)
+      for (const double f : fractions) {
+        Rng prng = master.split(201 + k++);
+        const PriorMatrix priors = prior_perturbation_protocol(truth, bd, pr, f, prng);
+        const McmcResult run = run_mcmc(data, cfg, priors, &cache);
+        row("priors", pr.first, pr.second, f, confusion(run.tracker.best().dag, truth),
+            run.tracker.best_score());
+      }
   });
 }
 

@@ -118,6 +118,20 @@ def chain_record(result, n: int) -> np.ndarray:
     return rec
 
 
+def chain_records_from_batch(batch, seeds, n: int) -> np.ndarray:
+    """chain_record for every chain of a ChainBatch (api.run_chains_batch)."""
+    seeds = np.asarray(seeds, np.uint64)
+    C_ = seeds.size
+    rec = np.zeros((C_, 4 + 2 * n), dtype=np.int64)
+    rec[:, 0] = seeds.view(np.int64)
+    rec[:, 1] = np.asarray(batch.accepted, np.uint64).view(np.int64)
+    rec[:, 2] = np.ascontiguousarray(batch.tracker_totals[:, 0], np.float64).view(np.int64)
+    rec[:, 3] = np.ascontiguousarray(batch.final_score, np.float64).view(np.int64)
+    rec[:, 4:4 + n] = np.ascontiguousarray(batch.tracker_masks[:, 0, :], np.uint64).view(np.int64)
+    rec[:, 4 + n:] = np.asarray(batch.final_order, np.int64)
+    return rec
+
+
 def decode_record(rec: np.ndarray, n: int) -> dict:
     return dict(seed=int(rec[0].view(np.uint64)), accepted=int(rec[1]),
                 best_total=float(rec[2:3].view(np.float64)[0]),

@@ -89,3 +89,26 @@ def test_chain_seeds_are_global_ids():
     s = [D.chain_seeds(1, r, 4, step=k, world=2) for k in range(2) for r in range(2)]
     flat = np.concatenate(s)
     assert list(flat) == list(range(1, 17))
+
+
+def test_chain_records_from_batch_roundtrip():
+    """The bench's per-chain records (ChainBatch -> fixed-size int64 records)
+    decode back to the batch's values; best_overall picks the best chain."""
+    from paper_1210_5128_b200.api import ChainBatch
+    n, C_, K, I = 5, 4, 3, 2
+    rng = np.random.default_rng(0)
+    b = ChainBatch(np.zeros((C_, I)), np.zeros((C_, I), np.uint8), np.zeros((C_, I)),
+                   np.stack([rng.permutation(n) for _ in range(C_)]).astype(np.int32),
+                   rng.normal(size=C_) - 10, np.arange(C_, dtype=np.uint64) * 7,
+                   np.full(C_, K, np.int32), rng.integers(0, 1 << 62, (C_, K, n)).astype(np.uint64),
+                   -np.sort(rng.random((C_, K)))[:, ::-1] * 0 - rng.random((C_, 1)) * 100,
+                   0.0, 0.0)
+    seeds = np.arange(11, 11 + C_, dtype=np.uint64)
+    rec = D.chain_records_from_batch(b, seeds, n)
+    for c in range(C_):
+        d = D.decode_record(rec[c], n)
+        assert d["seed"] == 11 + c and d["accepted"] == 7 * c
+        assert d["best_total"] == b.tracker_totals[c, 0] and d["final_score"] == b.final_score[c]
+        np.testing.assert_array_equal(d["best_masks"], b.tracker_masks[c, 0])
+        np.testing.assert_array_equal(d["final_order"], b.final_order[c])
+    assert D.best_overall(rec, n)["seed"] == 11 + int(np.argmax(b.tracker_totals[:, 0]))
