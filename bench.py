@@ -246,7 +246,7 @@ def run_ours(args):
             ours1 = P.run_chains(cache, pri, [1], c1)[0]
             cpu = cpu_baseline(cache, pri, cfg, ours1.trace_proposed, args.cpu_iters, 1)
         if world == 1 and not args.no_extras:
-            c1 = P.RunConfig(max_parents=cfg.max_parents, iterations=I, scan_mode=2, team_warps=8,
+            c1 = P.RunConfig(max_parents=cfg.max_parents, iterations=I, scan_mode=2, team_warps=0,
                              memory_cap_bytes=cfg.memory_cap_bytes, device=local)
             one = P.run_chains_batch(cache, pri, [1], c1)
             extra["single_chain_it_s"] = I / (one.device_ms / 1e3)

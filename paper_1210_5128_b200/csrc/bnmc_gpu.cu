@@ -506,7 +506,7 @@ void ensure_sorted(bnmc_table* t) {
   const uint64_t N = static_cast<uint64_t>(t->n) * t->S;
   // sorted rows padded with never-admissible entries so walk rounds need no
   // bounds checks: row stride Sw >= S + one full round
-  t->Sw = (t->S + 32 * kWalkUnroll + 31) / 32 * 32;
+  t->Sw = (t->S + 32 * kWalkPadRound + 31) / 32 * 32;
   const uint64_t NW = static_cast<uint64_t>(t->n) * t->Sw;
   t->seff.alloc(NW);
   t->scm.alloc(NW);
@@ -549,15 +549,19 @@ void launch_walk(bnmc_table* t, const WalkArgs& A, int C, int team_warps = 0) {
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, t->dev);
   int tw = team_warps;
-  if (tw == 0) tw = C <= 4 * sms ? 8 : (C <= 8 * sms ? 4 : (C <= 16 * sms ? 2 : 1));
-  const int per = kWalkThreads / (32 * tw);
+  if (tw == 0)
+    tw = C <= sms ? 32 : (C <= 4 * sms ? 8 : (C <= 8 * sms ? 4 : (C <= 16 * sms ? 2 : 1)));
+  const int cta = std::max(kWalkThreads, 32 * tw);
+  const int per = cta / (32 * tw);
   const unsigned grid = static_cast<unsigned>((C + per - 1) / per);
   switch (tw) {
-    case 8: walk_chain_kernel<8><<<grid, kWalkThreads, 0, t->stream>>>(A); break;
-    case 4: walk_chain_kernel<4><<<grid, kWalkThreads, 0, t->stream>>>(A); break;
-    case 2: walk_chain_kernel<2><<<grid, kWalkThreads, 0, t->stream>>>(A); break;
-    case 1: walk_chain_kernel<1><<<grid, kWalkThreads, 0, t->stream>>>(A); break;
-    default: raise(BNMC_USAGE, "team_warps must be 0, 1, 2, 4 or 8");
+    case 32: walk_chain_kernel<32><<<grid, cta, 0, t->stream>>>(A); break;
+    case 16: walk_chain_kernel<16><<<grid, cta, 0, t->stream>>>(A); break;
+    case 8: walk_chain_kernel<8><<<grid, cta, 0, t->stream>>>(A); break;
+    case 4: walk_chain_kernel<4><<<grid, cta, 0, t->stream>>>(A); break;
+    case 2: walk_chain_kernel<2><<<grid, cta, 0, t->stream>>>(A); break;
+    case 1: walk_chain_kernel<1><<<grid, cta, 0, t->stream>>>(A); break;
+    default: raise(BNMC_USAGE, "team_warps must be 0, 1, 2, 4, 8, 16 or 32");
   }
   CK(cudaGetLastError());
   t->last_team = tw;

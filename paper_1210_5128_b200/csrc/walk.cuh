@@ -38,6 +38,7 @@ constexpr int kWalkWarps = kWalkThreads / 32;
 #define BNMC_WALK_UNROLL 4
 #endif
 constexpr int kWalkUnroll = BNMC_WALK_UNROLL;  // entries per lane per (deep) walk round
+constexpr int kWalkPadRound = kWalkUnroll > 8 ? kWalkUnroll : 8;  // largest round of any variant
 #ifndef BNMC_WALK_MINB1
 #define BNMC_WALK_MINB1 4
 #endif
@@ -243,6 +244,7 @@ struct PairOut {
 // first maximum wins, as scan_slice + argmax_reduce). ins >= 0 inserts that
 // position into every listed subset (the listed subsets then range over the
 // other positions): used to enumerate only the sets containing one node.
+template <int EU>
 __device__ __forceinline__ PairOut enum_pst(const WalkArgs& A, int v, const uint64_t* __restrict__ pst, uint32_t cnt,
                             int ins, const uint8_t* order, const uint64_t* bt, const uint64_t* boff) {
   const int lane = threadIdx.x & 31;
@@ -251,11 +253,11 @@ __device__ __forceinline__ PairOut enum_pst(const WalkArgs& A, int v, const uint
   double best = -INFINITY;
   uint32_t bj = 0xFFFFFFFFu;
   bool dup = false;
-  for (uint32_t j0 = 0; j0 < cnt; j0 += 32 * kEnumUnroll) {
-    uint64_t nm[kEnumUnroll];
-    double lv[kEnumUnroll];
+  for (uint32_t j0 = 0; j0 < cnt; j0 += 32 * EU) {
+    uint64_t nm[EU];
+    double lv[EU];
 #pragma unroll
-    for (int u = 0; u < kEnumUnroll; ++u) {
+    for (int u = 0; u < EU; ++u) {
       const uint32_t j = j0 + u * 32 + lane;
       nm[u] = 0;
       lv[u] = -INFINITY;
@@ -268,7 +270,7 @@ __device__ __forceinline__ PairOut enum_pst(const WalkArgs& A, int v, const uint
       }
     }
 #pragma unroll
-    for (int u = 0; u < kEnumUnroll; ++u) {
+    for (int u = 0; u < EU; ++u) {
       const uint32_t j = j0 + u * 32 + lane;
       if (j >= cnt) continue;
       const double e = lv[u];  // ls + PpfTable::sum, precomputed (eff64_kernel)
@@ -314,6 +316,7 @@ struct DeltaIn {
 // Warp-cooperative exact argmax of row v for the node at position p whose
 // predecessors are `cpred` (candidate positions). order[pos] = node, ppos[node]
 // = pos of the order being scored; bt = binomial table in shared memory.
+template <int EU, int WU>
 __device__ PairOut pair_argmax(const WalkArgs& A, int v, int p, uint64_t cpred, const uint8_t* order,
                                const uint8_t* ppos, const uint64_t* bt, const uint64_t* boff,
                                const DeltaIn& d, unsigned long long* walked,
@@ -325,7 +328,7 @@ __device__ PairOut pair_argmax(const WalkArgs& A, int v, int p, uint64_t cpred, 
     // inserted); otherwise every admissible set (PST(p, s))
     const uint64_t* pst = d.on ? A.pst2 + A.pst2_off[p - 1] : A.pst + A.pst_off[p];
     const uint32_t cnt = d.on ? A.pst2_off[p] - A.pst2_off[p - 1] : A.pst_off[p + 1] - A.pst_off[p];
-    r = enum_pst(A, v, pst, cnt, d.on ? d.ypos : -1, order, bt, boff);
+    r = enum_pst<EU>(A, v, pst, cnt, d.on ? d.ypos : -1, order, bt, boff);
     if (lane == 0) *enumerated += cnt;
     if (d.on) {
       if (!(r.eff >= d.old_eff)) {  // also covers cnt == 0 (s == 0)
@@ -351,7 +354,7 @@ __device__ PairOut pair_argmax(const WalkArgs& A, int v, int p, uint64_t cpred, 
   if (walk_round<1>(re, rc, ncp, S, base, lane, h) || walk_round<2>(re, rc, ncp, S, base, lane, h) ||
       walk_round<4>(re, rc, ncp, S, base, lane, h)) {
   } else {
-    while (base < S && !walk_round<kWalkUnroll>(re, rc, ncp, S, base, lane, h)) {
+    while (base < S && !walk_round<WU>(re, rc, ncp, S, base, lane, h)) {
     }
   }
   const uint64_t start = h.start;
@@ -436,9 +439,10 @@ __device__ __forceinline__ void tracker_offer_warp(uint64_t* tm, double* tt, int
 // Barrier over the TW warps of one team (a team runs one chain).
 template <int TW>
 __device__ __forceinline__ void team_sync(int team) {
+  constexpr int kCta = TW * 32 > kWalkThreads ? TW * 32 : kWalkThreads;
   if constexpr (TW == 1) {
     __syncwarp();
-  } else if constexpr (TW * 32 == kWalkThreads) {
+  } else if constexpr (TW * 32 == kCta) {
     __syncthreads();
   } else {
     asm volatile("bar.sync %0, %1;" ::"r"(team + 1), "r"(TW * 32) : "memory");
@@ -461,22 +465,30 @@ struct TeamState {
   int np, a, b, accept, tcount, amb;
 };
 
-// TW warps per chain, kWalkThreads / (32 TW) chains per CTA. TW = 8 gives one
-// chain the whole CTA (lowest latency per iteration); TW = 1 runs a chain per
-// warp, barrier-free, for throughput over many chains.
 template <int TW>
-__global__ void __launch_bounds__(kWalkThreads, TW == 1 ? kWalkMinBlocks1 : 4) walk_chain_kernel(WalkArgs A) {
-  constexpr int kTeams = kWalkThreads / (32 * TW);
+__host__ __device__ constexpr int walk_cta_threads() {
+  return TW * 32 > kWalkThreads ? TW * 32 : kWalkThreads;
+}
+
+// TW warps per chain, max(256, 32 TW) / (32 TW) chains per CTA. TW >= 8 gives
+// one chain the whole CTA (lower latency per iteration); TW = 1 runs a chain
+// per warp, barrier-free, for throughput over many chains.
+
+template <int TW>
+__global__ void __launch_bounds__(walk_cta_threads<TW>(), TW == 1 ? kWalkMinBlocks1 : (TW > 8 ? 1024 / (TW * 32) : 4))
+    walk_chain_kernel(WalkArgs A) {
+  constexpr int kCta = walk_cta_threads<TW>();
+  constexpr int kTeams = kCta / (32 * TW);
   __shared__ uint64_t s_bt[65 * 9];
   __shared__ uint64_t s_boff[9];  // size-class offsets of global_index for c = n - 1
-  __shared__ unsigned long long s_stat[kWalkWarps][2];  // per warp: walked, enumerated
+  __shared__ unsigned long long s_stat[kCta / 32][2];  // per warp: walked, enumerated
   __shared__ TeamState s_team[kTeams];
   const int tid = threadIdx.x, lane = tid & 31;
   const int team = (tid >> 5) / TW, twarp = (tid >> 5) % TW, ttid = tid - team * TW * 32;
   const int c = blockIdx.x * kTeams + team;
   const int n = A.n;
-  for (int i = tid; i < 65 * 9; i += kWalkThreads) s_bt[i] = binom(i / 9, i % 9);
-  if (tid < 2 * kWalkWarps) (&s_stat[0][0])[tid] = 0;
+  for (int i = tid; i < 65 * 9; i += kCta) s_bt[i] = binom(i / 9, i % 9);
+  if (tid < 2 * (kCta / 32)) (&s_stat[0][0])[tid] = 0;
   if (tid < 9) {
     uint64_t o = 0;
     for (int j = tid + 1; j <= A.s; ++j) o += binom(A.n - 1, j);
@@ -604,7 +616,8 @@ __global__ void __launch_bounds__(kWalkThreads, TW == 1 ? kWalkMinBlocks1 : 4) w
       d.ypos = lo;
       d.old_eff = S.cb[v];
       d.old_cm = nodes_to_cand(S.cm[v], v);
-      const PairOut o = pair_argmax(A, v, S.pp[q], S.pc[q], S.prop, S.ppos, s_bt, s_boff, d,
+      // few chains in flight (TW >= 8): more independent gathers per lane
+      const PairOut o = pair_argmax<TW >= 8 ? 4 : kEnumUnroll, TW >= 8 ? 8 : kWalkUnroll>(A, v, S.pp[q], S.pc[q], S.prop, S.ppos, s_bt, s_boff, d,
                                     walked, enumerated);
       if (lane == 0) {
         S.pm[v] = cand_to_nodes(o.cm, v);
