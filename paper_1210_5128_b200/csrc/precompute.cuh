@@ -27,6 +27,8 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
+#include <cstring>
 #include <set>
 #include <vector>
 
@@ -38,6 +40,7 @@ namespace bnmc_dev {
 constexpr int kHMax = 4096;   // max joint cells of a set U (dense counter bound)
 constexpr int kRPMax = 1024;  // max configurations of a prefix P
 constexpr int kK1Threads = 256;
+constexpr int kMaxPrefix = 8;  // members of a prefix P (|P| <= s <= 8)
 
 struct K1Args {
   const uint32_t* __restrict__ bits;  // bitplanes
@@ -111,6 +114,7 @@ __device__ __forceinline__ int find_pair(const K1Args& a, uint64_t key) {
   return -1;
 }
 
+template <bool TILED>
 __global__ void __launch_bounds__(kK1Threads) k1_kernel(K1Args a, uint64_t prefix_base) {
   extern __shared__ uint32_t smem[];
   __shared__ int s_p[9];
@@ -146,10 +150,39 @@ __global__ void __launch_bounds__(kK1Threads) k1_kernel(K1Args a, uint64_t prefi
     return;
   }
   const int cmax = a.cmax;
-  const int WT = a.WT;
-  uint32_t* PB = smem;                         // [rP][WT]
-  uint32_t* NP = PB + (size_t)rP * WT;         // [rP]
+  const int WT = TILED ? a.WT : 0;             // AND-plane tiles in smem, or formed on the fly
+  const int WTP = WT | 1;                      // odd row stride: lanes over cfgs hit distinct banks
+  uint32_t* NP = smem;                         // [rP]
   uint32_t* CNT = NP + rP;                     // [EG][rP][cmax]
+  uint32_t* PB = CNT + (size_t)a.EG * rP * cmax;  // [rP][WTP] (tiled mode)
+  uint32_t* PO = PB + (size_t)rP * WTP;        // [rP][kMaxPrefix] member plane offsets (tiled)
+  const int warp = tid >> 5, lane = tid & 31;
+  const int nx = cmax - 1;
+  const int ncg = (rP + 31) / 32;
+
+  // Member plane rows of configuration cfg of P (mixed radix, lowest member
+  // least significant, scoring.cpp:99-105).
+  auto member_rows = [&](int cfg, const uint32_t** mp) {
+    int rem = cfg < rP ? cfg : 0;
+#pragma unroll
+    for (int i = 0; i < kMaxPrefix; ++i) {
+      if (i < k) {
+        const int ci = a.cards[s_p[i]];
+        mp[i] = a.bits + a.boff[s_p[i]] + (uint32_t)(rem % ci) * W;
+        rem /= ci;
+      } else {
+        mp[i] = nullptr;
+      }
+    }
+  };
+
+  if constexpr (TILED) {
+    for (int cfg = tid; cfg < rP; cfg += kK1Threads) {
+      const uint32_t* mp[kMaxPrefix];
+      member_rows(cfg, mp);
+      for (int i = 0; i < k; ++i) PO[cfg * kMaxPrefix + i] = (uint32_t)(mp[i] - a.bits);
+    }
+  }
 
   for (int e0 = 0; e0 < n_ext; e0 += a.EG) {
     const int ne = min(a.EG, n_ext - e0);
@@ -157,41 +190,67 @@ __global__ void __launch_bounds__(kK1Threads) k1_kernel(K1Args a, uint64_t prefi
     if (e0 == 0)
       for (int i = tid; i < rP; i += kK1Threads) NP[i] = 0;
     __syncthreads();
-    for (int w0 = 0; w0 < W; w0 += WT) {
-      const int wt = min(WT, W - w0);
-      // AND-planes of every configuration of P over this word tile.
-      for (int idx = tid; idx < rP * wt; idx += kK1Threads) {
-        const int cfg = idx / wt, w = idx - cfg * wt;
-        uint32_t word = (w0 + w == W - 1) ? a.last_mask : 0xFFFFFFFFu;
-        int rem = cfg;
-        for (int i = 0; i < k; ++i) {
-          const int ci = a.cards[s_p[i]];
-          const int d = rem % ci;
-          rem /= ci;
-          word &= a.bits[a.boff[s_p[i]] + (uint32_t)d * W + w0 + w];
+    // Counting as a popcount "product": a lane owns one configuration of P,
+    // a warp unit owns 32 configurations x 4 (extension, state) planes read as
+    // warp-broadcast loads; every output belongs to one lane (no atomics). The
+    // configuration's AND-plane comes from a shared-memory tile (tiled mode)
+    // or is formed word by word from its member planes (WT == 0; few distinct
+    // addresses per warp load). The last state of u comes by difference below.
+    const int nex = ne * nx;
+    const int units = ncg * ((nex + 3) / 4) + (e0 == 0 ? ncg : 0);
+    const int tile = WT > 0 ? WT : W;
+    for (int w0 = 0; w0 < W; w0 += tile) {
+      const int wt = min(tile, W - w0);
+      if constexpr (TILED) {
+        for (int idx = tid; idx < rP * wt; idx += kK1Threads) {
+          const int cfg = idx / wt, w = idx - cfg * wt;
+          uint32_t word = (w0 + w == W - 1) ? a.last_mask : 0xFFFFFFFFu;
+          for (int i = 0; i < k; ++i) word &= __ldg(a.bits + PO[cfg * kMaxPrefix + i] + w0 + w);
+          PB[cfg * WTP + w] = word;
         }
-        PB[cfg * WT + w] = word;
+        __syncthreads();
       }
-      __syncthreads();
-      const int NS = max(1, min(wt, kK1Threads / rP));
-      for (int task = tid; task < rP * NS; task += kK1Threads) {
-        const int cfg = task % rP, sl = task / rP;
-        const int wa = sl * wt / NS, wb = (sl + 1) * wt / NS;
-        const uint32_t* pb = PB + cfg * WT;
-        if (e0 == 0) {
+      for (int un = warp; un < units; un += kK1Threads / 32) {
+        const int cg = un % ncg, blk = un / ncg;
+        const int cfg = cg * 32 + lane;
+        const uint32_t* mp[kMaxPrefix];
+        if constexpr (!TILED) member_rows(cfg, mp);
+        const uint32_t* pb = PB + (cfg < rP ? cfg : 0) * WTP;
+        auto plane_word = [&](int w) -> uint32_t {
+          if constexpr (TILED) return pb[w];
+          uint32_t pw = w0 + w == W - 1 ? a.last_mask : 0xFFFFFFFFu;
+#pragma unroll
+          for (int i = 0; i < kMaxPrefix; ++i)
+            if (i < k) pw &= __ldg(mp[i] + w0 + w);
+          return pw;
+        };
+        if (blk * 4 >= nex) {  // prefix counts (first extension group only)
           uint32_t acc = 0;
-          for (int w = wa; w < wb; ++w) acc += __popc(pb[w]);
-          atomicAdd(&NP[cfg], acc);
+          for (int w = 0; w < wt; ++w) acc += __popc(plane_word(w));
+          if (cfg < rP) NP[cfg] += acc;
+          continue;
         }
-        for (int e = 0; e < ne; ++e) {
-          const int u = ext0 + e0 + e;
-          const int cu = a.cards[u];
-          for (int x = 0; x < cu - 1; ++x) {
-            const uint32_t* bp = a.bits + a.boff[u] + (uint32_t)x * W + w0;
-            uint32_t acc = 0;
-            for (int w = wa; w < wb; ++w) acc += __popc(pb[w] & __ldg(bp + w));
-            atomicAdd(&CNT[(e * rP + cfg) * cmax + x], acc);
-          }
+        const uint32_t* bp[4];
+        int slot[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int ex = blk * 4 + q;
+          const int e = ex / nx, x = ex - e * nx;
+          const int u = ext0 + e0 + (e < ne ? e : 0);
+          const bool ok = ex < nex && x < a.cards[u] - 1;
+          slot[q] = ok ? (e * rP + cfg) * cmax + x : -1;
+          bp[q] = a.bits + a.boff[u] + (uint32_t)(ok ? x : 0) * W + w0;
+        }
+        uint32_t acc[4] = {0, 0, 0, 0};
+        for (int w = 0; w < wt; ++w) {
+          const uint32_t pw = plane_word(w);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) acc[q] += __popc(pw & __ldg(bp[q] + w));
+        }
+        if (cfg < rP) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (slot[q] >= 0) CNT[slot[q]] += acc[q];
         }
       }
       __syncthreads();
@@ -468,15 +527,37 @@ inline void precompute_rows(cudaStream_t stream, double* d_ls, uint64_t S, const
   a.S = S;
   a.row_begin = row_begin;
   a.row_end = row_end;
-  // Shared memory: PB tile + NP + CNT for a group of extensions.
-  const size_t budget = 200 * 1024;
+  // Shared memory, sized for several CTAs per SM so one CTA's scoring phase
+  // overlaps other CTAs' counting: prefix counts + CNT for a group of
+  // extensions (+ an AND-plane word tile in tiled mode). Tiled mode re-forms
+  // the tile once per extension group, so it is used when one group covers
+  // a typical prefix's extensions; otherwise AND-planes are formed on the fly.
+  const char* kb = std::getenv("BNMC_K1_SMEM_KB");
+  const size_t budget = (kb ? std::strtoul(kb, nullptr, 10) : 48) * 1024;
   const int rPmax = static_cast<int>(hp);
-  a.EG = std::max(1, std::min(n, static_cast<int>((64 * 1024) / (4ull * rPmax * cmax))));
-  const size_t cnt_bytes = 4ull * a.EG * rPmax * cmax + 4ull * rPmax;
-  a.WT = std::max(1, std::min(std::max(bp.W, 1), static_cast<int>((budget - cnt_bytes) / (4ull * rPmax))));
+  const size_t np_bytes = 4ull * rPmax;
+  const int wt_fit = static_cast<int>((budget / 2) / (4ull * rPmax)) - 1;
+  int wt = std::max(1, std::min(std::max(bp.W, 1), std::max(32, wt_fit)));
+  size_t pb_bytes = 4ull * rPmax * (wt | 1);
+  size_t left = budget > pb_bytes + np_bytes ? budget - pb_bytes - np_bytes : 0;
+  int eg = static_cast<int>(left / (4ull * rPmax * cmax));
+  const char* mode = std::getenv("BNMC_K1_MODE");  // "tiled" / "fly" (development)
+  const bool tiled = mode ? std::strcmp(mode, "tiled") == 0 : eg >= std::min(n, 16);
+  if (!tiled) {
+    wt = 0;
+    pb_bytes = 0;
+    left = budget > np_bytes ? budget - np_bytes : 0;
+    eg = static_cast<int>(left / (4ull * rPmax * cmax));
+  }
+  a.WT = wt;
+  a.EG = std::max(1, std::min(n, eg));
+  const size_t cnt_bytes = 4ull * a.EG * rPmax * cmax + np_bytes + pb_bytes +
+                           (tiled ? 4ull * rPmax * kMaxPrefix : 0);
   a.error = d_err;
-  const size_t shm = 4ull * rPmax * a.WT + cnt_bytes;
-  CK(cudaFuncSetAttribute(k1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  const size_t shm = cnt_bytes;
+  CK(cudaFuncSetAttribute(k1_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          static_cast<int>(shm)));
+  CK(cudaFuncSetAttribute(k1_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           static_cast<int>(shm)));
   const uint64_t prefixes = [&] {
     uint64_t t = 0;
@@ -494,7 +575,10 @@ inline void precompute_rows(cudaStream_t stream, double* d_ls, uint64_t S, const
   const uint64_t chunk = 1u << 30;
   for (uint64_t base = 0; base < prefixes; base += chunk) {
     const unsigned blocks = static_cast<unsigned>(std::min(chunk, prefixes - base));
-    k1_kernel<<<blocks, kK1Threads, shm, stream>>>(a, base);
+    if (tiled)
+      k1_kernel<true><<<blocks, kK1Threads, shm, stream>>>(a, base);
+    else
+      k1_kernel<false><<<blocks, kK1Threads, shm, stream>>>(a, base);
     CK(cudaGetLastError());
   }
   CK(cudaEventRecord(e1, stream));
