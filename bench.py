@@ -102,6 +102,17 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
+def ncu_traffic(kernel):
+    """DRAM bytes per launch of `kernel` from the committed ncu capture
+    (profiles/ncu_traffic.json, written from an ncu --set full report of this
+    bench's configuration), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            return float(json.load(f)[kernel]["dram_bytes_per_launch"])
+    except Exception:
+        return None
+
+
 def flush_l2(torch, buf):
     buf.add_(1.0)  # 256 MiB write > 126 MB L2
 
@@ -270,13 +281,15 @@ def run_ours(args):
                     "note": "bnmc_gpu_run_chains with host seeds in, pinned host trace/tracker/"
                             "final-state buffers out; wall time per call"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None,
+                         "frac": achieved / peak, "traffic": ncu_traffic("walk_chain_kernel"),
                          "kernel": "walk_chain_kernel (K2W: fused scan + chain step)",
                          "peak_source": peak_src, "bytes_per_launch": bytes_per_launch,
                          "avg_launch_us": avg_launch_s * 1e6,
                          "note": "algorithmic bytes = sorted entries walked x 16 B + PST-enumerated "
                                  "local scores x 8 B; the touched tops of the sorted rows are "
-                                 "L2-resident, so the kernel is latency/issue-bound, not HBM-bound"},
+                                 "L2-resident (traffic = ncu DRAM bytes per launch, well below the "
+                                 "algorithmic bytes), so the kernel is latency/issue-bound, not "
+                                 "HBM-bound"},
             "walk": {"pairs_per_iteration": pairs / (args.steps * Cn * (I + 1)),
                      "walked_per_pair": walked / max(1, pairs),
                      "enumerated_per_pair": enumerated / max(1, pairs),

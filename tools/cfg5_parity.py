@@ -1,0 +1,85 @@
+"""cfg5-scale parity (SURVEY §8d "cfg5"): n=64, k=5, m=20000, 3-state, priors.
+
+The reference's CPU precompute at this scale takes hours, so parity is pinned
+the way SURVEY §8d prescribes:
+  * 10,000 sampled (node, parent set) local scores of the GPU-built table vs
+    the reference's local_score (bit-exact);
+  * the GPU table exported as BNSC and read by the reference's ScoreCache::load;
+    OrderScorer::score on random orders (reference, all host threads) vs the
+    device scan (masks and totals bit-exact);
+  * a short chain: reference run_mcmc on the loaded cache vs the device chain
+    with the same seed (trace, tracker, final state bit-exact).
+Prints one JSON object (committed as profiles/r01_cfg5_parity.json).
+  python tools/cfg5_parity.py [iterations] [orders]
+"""
+import json
+import os
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_1210_5128_b200 as P  # noqa: E402
+from oracle import ref  # noqa: E402
+
+iters = int(sys.argv[1]) if len(sys.argv) > 1 else 20
+n_orders = int(sys.argv[2]) if len(sys.argv) > 2 else 4
+out = {"config": "cfg5: n=64 k=5 m=20000 3-state + pairwise priors (seed 7)"}
+data, pri, cfg, truth = P.baseline_instance("cfg5")
+t0 = time.perf_counter()
+cache = P.ScoreCache.build(data, cfg, pri)
+out["gpu_build_s"] = time.perf_counter() - t0
+out["gpu_k1_ms"] = cache.build_ms[0]
+S = cache.entries_per_node()
+table = cache.table()
+
+rng = np.random.default_rng(5)
+samp_ok, t0 = 0, time.perf_counter()
+NS = 10000
+for _ in range(NS):
+    v = int(rng.integers(0, data.n))
+    g = int(rng.integers(0, S))
+    cm = ref.subset_at(g, data.n - 1, cfg.max_parents)
+    low = cm & ((1 << v) - 1)
+    pset = low | ((cm >> v) << (v + 1))
+    r = ref.local_score(data.cells, data.cards, v, pset)
+    samp_ok += int(np.float64(r).view(np.uint64) == table[v, g].view(np.uint64))
+out["sampled_entries_bit_exact"] = f"{samp_ok}/{NS}"
+out["cpu_local_score_s_per_entry"] = (time.perf_counter() - t0) / NS
+
+with tempfile.TemporaryDirectory(dir=os.environ.get("BNMC_TMP", "/tmp")) as d:
+    path = os.path.join(d, "cfg5.bnsc")
+    t0 = time.perf_counter()
+    cache.save(path)
+    rc = ref.Cache.load(path, cfg.max_parents, cfg.gamma, cfg.ess, False)
+    out["bnsc_roundtrip_s"] = time.perf_counter() - t0
+del table
+perms = np.stack([rng.permutation(data.n) for _ in range(n_orders)]).astype(np.int32)
+masks, best, tot = P.OrderScorer(cache, pri).score_many(perms)
+scorer = ref.Scorer(rc, pri)
+ok, t0 = 0, time.perf_counter()
+for i in range(n_orders):
+    m, t = scorer.score(perms[i])
+    ok += int(np.array_equal(m, masks[i]) and t == tot[i])
+out["orders_bit_exact"] = f"{ok}/{n_orders}"
+out["cpu_order_score_s"] = (time.perf_counter() - t0) / n_orders
+out["cpu_threads"] = ref.max_threads()
+
+cfg.iterations, cfg.seed = iters, 1
+ours = P.run_mcmc(data, cfg, pri, prebuilt=cache)
+t0 = time.perf_counter()
+r = ref.run_mcmc(np.zeros((1, data.n), np.uint8), np.full(data.n, 3, np.int32), cfg.max_parents,
+                 iters, 1, priors=pri, prebuilt=rc)
+out["cpu_chain_s"] = time.perf_counter() - t0
+out["chain_iterations"] = iters
+out["chain_trace_bit_exact"] = bool(np.array_equal(ours.trace_proposed, r.trace_proposed)
+                                    and np.array_equal(ours.trace_accepted, r.trace_accepted)
+                                    and np.array_equal(ours.trace_best, r.trace_best))
+out["chain_tracker_bit_exact"] = bool(np.array_equal(ours.tracker_masks, r.tracker_masks)
+                                      and np.array_equal(ours.tracker_totals, r.tracker_totals))
+out["chain_final_state_equal"] = bool(np.array_equal(ours.final_order, r.final_order)
+                                      and ours.final_score == r.final_score
+                                      and ours.accepted == r.accepted)
+print(json.dumps(out), flush=True)
