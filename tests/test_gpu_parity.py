@@ -149,3 +149,42 @@ def test_cfg4_golden(mode, golden, golden_meta):
     np.testing.assert_array_equal(r.trace_proposed, g["trace_proposed"])
     np.testing.assert_array_equal(r.tracker_masks, g["tracker_masks"])
     assert r.accepted == meta["accepted"] and r.final_score == meta["final_score"]
+
+
+def test_cfg5_scale_parity_via_bnsc(tmp_path):
+    """BASELINE cfg5 (n=64, k=5, m=20000): the reference's precompute takes hours,
+    so parity is pinned as SURVEY §8d prescribes — sampled local scores vs the
+    reference's local_score, the GPU table read by the reference's
+    ScoreCache::load, order scores and a short chain vs the reference on it."""
+    from oracle import ref
+    if not ref.available():
+        pytest.skip("oracle/_ref not built")
+    data, pri, cfg = instance("cfg5")
+    cache = P.ScoreCache.build(data, cfg, pri)
+    S = cache.entries_per_node()
+    t = cache.table()
+    rng = np.random.default_rng(11)
+    for _ in range(300):
+        v, g = int(rng.integers(0, data.n)), int(rng.integers(0, S))
+        cm = ref.subset_at(g, data.n - 1, cfg.max_parents)
+        pset = (cm & ((1 << v) - 1)) | ((cm >> v) << (v + 1))
+        r = ref.local_score(data.cells, data.cards, v, pset)
+        assert np.float64(r).view(np.uint64) == t[v, g].view(np.uint64)
+    del t
+    path = str(tmp_path / "cfg5.bnsc")
+    cache.save(path)
+    rc = ref.Cache.load(path, cfg.max_parents, cfg.gamma, cfg.ess, False)
+    perms = np.stack([rng.permutation(data.n) for _ in range(2)]).astype(np.int32)
+    masks, best, tot = P.OrderScorer(cache, pri).score_many(perms)
+    sc = ref.Scorer(rc, pri)
+    for i in range(2):
+        m, tt = sc.score(perms[i])
+        np.testing.assert_array_equal(masks[i], m)
+        assert tot[i] == tt
+    cfg.iterations, cfg.seed = 8, 3
+    ours = P.run_mcmc(data, cfg, pri, prebuilt=cache)
+    r = ref.run_mcmc(np.zeros((1, data.n), np.uint8), np.full(data.n, 3, np.int32),
+                     cfg.max_parents, 8, 3, priors=pri, prebuilt=rc)
+    np.testing.assert_array_equal(ours.trace_proposed, r.trace_proposed)
+    np.testing.assert_array_equal(ours.tracker_masks, r.tracker_masks)
+    assert ours.final_score == r.final_score
