@@ -174,7 +174,10 @@ def run_ours(args):
     rank, world, local = D.env_rank_world()
     torch.cuda.set_device(local)
     group = None
-    if world > 1:
+    # --force-dist exercises the multi-GPU code path (NCCL process group, row
+    # all-gather, record gather, max-over-ranks) even at world size 1
+    dist_on = world > 1 or args.force_dist
+    if dist_on:
         import torch.distributed as tdist
         tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
     data, pri, cfg, truth = P.baseline_instance(args.config)
@@ -182,7 +185,7 @@ def run_ours(args):
     # ---- precompute: row-sharded K1 + NCCL all-gather, then the per-row sort
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    cache = D.build_table_sharded(data, cfg, pri, rank, world, group)
+    cache = D.build_table_sharded(data, cfg, pri, rank, world, group, force=dist_on)
     cfg.iterations, cfg.scan_mode = 1, 2
     P.run_chains_batch(cache, pri, [1], cfg)  # binds priors, builds the sorted rows
     torch.cuda.synchronize()
@@ -204,7 +207,7 @@ def run_ours(args):
                            pinned((Cn, K), torch.float64), 0.0, 0.0)
     for w in range(args.warmup):
         P.run_chains_batch(cache, pri, D.chain_seeds(1000001, rank, Cn, w, world), cfg, out)
-    if world > 1:
+    if dist_on:
         import torch.distributed as tdist
         tdist.barrier()
     torch.cuda.synchronize()
@@ -229,7 +232,7 @@ def run_ours(args):
     tot_dev = sum(dev_ms) / 1e3
     tot_wall = sum(wall_s)
     recs = D.chain_records_from_batch(out, D.chain_seeds(1, rank, Cn, args.steps - 1, world), n)
-    if world > 1:
+    if dist_on:
         import torch.distributed as tdist
         tt = torch.tensor([tot_dev, tot_wall, pre_s], device="cuda", dtype=torch.float64)
         tdist.all_reduce(tt, op=tdist.ReduceOp.MAX)
@@ -302,7 +305,7 @@ def run_ours(args):
         }
         out_line.update(extra)
         print(json.dumps(out_line), flush=True)
-    if world > 1:
+    if dist_on:
         import torch.distributed as tdist
         tdist.barrier()
         tdist.destroy_process_group()
@@ -365,6 +368,8 @@ def main():
     ap.add_argument("--chains", type=int, default=18944, help="chains per GPU (128 per SM)")
     ap.add_argument("--team-warps", type=int, default=0, help="warps per chain (0 auto)")
     ap.add_argument("--no-extras", action="store_true", help="skip single-chain/full-scan probes")
+    ap.add_argument("--force-dist", action="store_true",
+                    help="run the multi-GPU code path (NCCL) even at world size 1")
     ap.add_argument("--iters", type=int, default=500, help="MCMC iterations per chain per step")
     ap.add_argument("--cpu-iters", type=int, default=200)
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -81,7 +81,7 @@ def all_gather_rows(rows, n: int, world: int, rank: int, group=None):
     return rows
 
 
-def build_table_sharded(data, cfg, priors, rank: int, world: int, group=None):
+def build_table_sharded(data, cfg, priors, rank: int, world: int, group=None, force=False):
     """Row-sharded device precompute + NCCL all-gather -> full table on every GPU."""
     from .api import ScoreCache, _prior_array
     import time
@@ -93,7 +93,7 @@ def build_table_sharded(data, cfg, priors, rank: int, world: int, group=None):
         data.cells.reshape(-1), data.cards, data.rows(), data.n, C.byref(cfg.score_params()),
         _lib.ptr(pr), a, b, C.byref(out)))
     cache = ScoreCache(out.value, data.n, cfg.max_parents, cfg)
-    if world > 1:
+    if world > 1 or force:
         import torch
         rows = table_rows_tensor(cache)
         torch.cuda.synchronize()
