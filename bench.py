@@ -153,11 +153,11 @@ def full_scan_probe(P, _lib, cache, pri, cfg, chains=64, iters=100):
     _lib.check(_lib.lib().bnmc_gpu_last_scan_stats(cache.handle, C.byref(a), C.byref(s_),
                                                     C.byref(t), C.byref(d)))
     launches = iters + 1
-    bpl = s_.value * 32.0 / launches
+    bpl = s_.value * 16.0 / launches  # 16-byte key slots streamed by K2
     avg = t.value / 1e3
     peak, src = load_peaks()
     return {"it_s": chains * iters / (b.device_ms / 1e3), "chains": chains, "iterations": iters,
-            "kernel": "scan_kernel (K2, full-row fp32-key scan)",
+            "kernel": "scan2_kernel (K2, full-row fp32-key scan)",
             "roofline": {"bound": "hbm", "achieved": bpl / avg / 1e9, "peak": peak, "unit": "GB/s",
                          "frac": bpl / avg / 1e9 / peak, "bytes_per_launch": bpl,
                          "avg_launch_us": avg * 1e6, "peak_source": src,

@@ -173,7 +173,7 @@ int bnmc_gpu_run_chains(bnmc_table* t, const uint64_t* seeds, int n_chains,
                         uint64_t* tracker_masks, double* tracker_totals, float* device_ms);
 
 /* Statistics of the last run_chains call: node-row rescans (summed over
- * chains and iterations), 32-byte key sectors streamed by the scan kernel
+ * chains and iterations), 16-byte key slots streamed by the scan kernel
  * (after batching chains per row and skipping sectors no pair can admit), the
  * average device time of one scan launch (CUDA events around every
  * timing_sample-th launch inside the loop, ms) and the number of kernel

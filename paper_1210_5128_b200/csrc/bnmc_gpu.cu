@@ -216,41 +216,30 @@ struct ScanGeom {
 // the row fits), RB rows per cp.async pipeline stage within the smem budget.
 ScanGeom scan_geometry(const bnmc_table* t, int max_pairs) {
   ScanGeom g;
+  (void)max_pairs;
   g.sectors = static_cast<int>(t->Sp / 8);
-  int sms = 148;
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, t->dev);
-  g.Ls = std::min(kMaxLs, (g.sectors + sms - 1) / sms);
-  g.Ls = std::max(1, g.Ls);
-  g.G = (g.sectors + g.Ls - 1) / g.Ls;
-  const size_t budget = 220 * 1024;
-  g.RB = 8;
-  while (g.RB > 1 && scan_smem_bytes(g.Ls, g.RB, max_pairs) > budget) --g.RB;
+  g.Ls = 0;
+  g.RB = 0;
+  const uint64_t slots = (static_cast<uint64_t>(g.sectors) * 8 + kScan2Per - 1) / kScan2Per;
+  g.G = static_cast<int>((slots + kScan2Threads - 1) / kScan2Threads);
   return g;
 }
 
+// K2 (scan2_kernel): one thread per 32-byte key sector of every row.
 void launch_scan(const ScanGeom& g, ScanArgs a, int max_pairs, cudaStream_t s, bool pdl) {
-  a.Ls = g.Ls;
-  a.RB = g.RB;
   a.sectors = g.sectors;
   a.max_pairs = max_pairs;
-  const size_t shm = scan_smem_bytes(g.Ls, g.RB, max_pairs);
-  static size_t configured = 0;
-  if (shm > configured) {
-    CK(cudaFuncSetAttribute(scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            static_cast<int>(std::max<size_t>(shm, 48 * 1024))));
-    configured = shm;
-  }
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(g.G);
-  cfg.blockDim = dim3(kScanThreads);
-  cfg.dynamicSmemBytes = shm;
+  cfg.gridDim = dim3(g.G, kScan2RowGroups);
+  cfg.blockDim = dim3(kScan2Threads);
+  cfg.dynamicSmemBytes = 0;
   cfg.stream = s;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  CK(cudaLaunchKernelEx(&cfg, scan_kernel, a));
+  CK(cudaLaunchKernelEx(&cfg, scan2_kernel, a));
 }
 
 void launch_step(int C, const StepArgs& A, cudaStream_t s, bool pdl) {
