@@ -185,6 +185,7 @@ struct bnmc_table {
   DevBuf<double> thr;
   DevBuf<uint64_t> tmasks;
   DevBuf<double> ttotals;
+  DevBuf<uint64_t> thash;
   DevBuf<double> tr_prop, tr_best;
   DevBuf<uint8_t> tr_acc;
   DevBuf<unsigned long long> stat;
@@ -700,6 +701,7 @@ void walk_launch(bnmc_table* t, const uint64_t* seeds, int C, const bnmc_chain_p
   t->seeds.alloc(C);
   t->tmasks.alloc(static_cast<size_t>(C) * K * n);
   t->ttotals.alloc(static_cast<size_t>(C) * K);
+  t->thash.alloc(static_cast<size_t>(C) * K);
   t->tr_prop.alloc(static_cast<size_t>(C) * iters);
   t->tr_best.alloc(static_cast<size_t>(C) * iters);
   t->tr_acc.alloc(static_cast<size_t>(C) * iters);
@@ -726,6 +728,7 @@ void walk_launch(bnmc_table* t, const uint64_t* seeds, int C, const bnmc_chain_p
   A.ambiguous = t->d_amb.p;
   A.tmasks = t->tmasks.p;
   A.ttotals = t->ttotals.p;
+  A.thash = t->thash.p;
   A.tcount = t->d_tc.p;
   A.tr_prop = t->tr_prop.p;
   A.tr_acc = t->tr_acc.p;

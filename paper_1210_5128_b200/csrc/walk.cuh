@@ -74,6 +74,7 @@ struct WalkArgs {
   int* ambiguous;                      // [C] set when a decision fell inside the bound
   uint64_t* tmasks;                    // [C][K][n]
   double* ttotals;                     // [C][K]
+  uint64_t* thash;                     // [C][K] graph hashes of the tracker entries
   int* tcount;                         // [C]
   double* tr_prop;                     // [C][iters]
   uint8_t* tr_acc;
@@ -107,14 +108,14 @@ __device__ __forceinline__ bool prefer_pos(uint64_t ma, uint64_t mb, int v, cons
 // bt[c * 9 + j] = C(c, j), j <= 8.
 __device__ __forceinline__ uint64_t gidx_smem(uint64_t mask, int c, const uint64_t* off,
                                               const uint64_t* bt) {
+  // Lexicographic rank of the sorted members a_1 < ... < a_k of {0..c-1} as
+  // C(c,k) - 1 - sum_t C(c-1-a_t, k-t+1) (one table lookup per member; equal to
+  // the telescoped sum of combinatorics.cpp:61-76), after the larger size
+  // classes off[k] = sum_{j>k} C(c, j).
   const int k = __popcll(mask);
-  uint64_t idx = off[k];  // sum_{j>k} C(c, j): the larger size classes come first
-  int prev = 0, i = 0;
-  for (uint64_t m = mask; m; m &= m - 1, ++i) {
-    const int a = __ffsll((long long)m);
-    idx += bt[(c - prev) * 9 + (k - i)] - bt[(c - a + 1) * 9 + (k - i)];
-    prev = a;
-  }
+  uint64_t idx = off[k] + bt[c * 9 + k] - 1;
+  int j = k;
+  for (uint64_t m = mask; m; m &= m - 1, --j) idx -= bt[(c - __ffsll((long long)m)) * 9 + j];
   return idx;
 }
 
@@ -385,15 +386,26 @@ __device__ PairOut pair_argmax(const WalkArgs& A, int v, int p, uint64_t cpred, 
 // BestGraphTracker::update (sampler.cpp:32-41) by one warp: dedupe by full
 // graph equality, reject when full and total <= the minimum, insert at the
 // lower bound of (total desc, Dag operator< over the parent masks).
-__device__ __noinline__ void tracker_insert_warp(uint64_t* tm, double* tt, int K, int n,
+__device__ __noinline__ void tracker_insert_warp(uint64_t* tm, double* tt, uint64_t* th, int K, int n,
                                                  const uint64_t* pm, double proposed, int* tcount) {
   const int lane = threadIdx.x & 31;
   const int count = *tcount;
   const bool full = count == K;
-  for (int e = 0; e < count; ++e) {
-    bool eq = true;
-    for (int i = lane; i < n; i += 32) eq &= tm[(uint64_t)e * n + i] == pm[i];
-    if (__all_sync(0xffffffffu, eq)) return;
+  // graph hash: dedupe compares hashes first, masks only on a hash match
+  uint64_t hv = 0;
+  for (int i = lane; i < n; i += 32) hv ^= Rng::mix(pm[i] + 0x9E3779B97F4A7C15ull * (uint64_t)(i + 1));
+  const uint64_t h = ((uint64_t)__reduce_xor_sync(0xffffffffu, (unsigned)(hv >> 32)) << 32) |
+                     __reduce_xor_sync(0xffffffffu, (unsigned)hv);
+  for (int e0 = 0; e0 < count; e0 += 32) {
+    const int e1 = e0 + lane;
+    unsigned cand = __ballot_sync(0xffffffffu, e1 < count && th[e1] == h);
+    while (cand) {
+      const int e = e0 + __ffs(cand) - 1;
+      cand &= cand - 1;
+      bool eq = true;
+      for (int i = lane; i < n; i += 32) eq &= tm[(uint64_t)e * n + i] == pm[i];
+      if (__all_sync(0xffffffffu, eq)) return;  // already tracked
+    }
   }
   int ins = 0;
   for (int e0 = 0; e0 < count; e0 += 32) {
@@ -418,22 +430,26 @@ __device__ __noinline__ void tracker_insert_warp(uint64_t* tm, double* tt, int K
   const int last = full ? count - 1 : count;
   for (int e = last; e > ins; --e) {  // move entries [ins, last) down one slot
     for (int i = lane; i < n; i += 32) tm[(uint64_t)e * n + i] = tm[(uint64_t)(e - 1) * n + i];
-    if (lane == 0) tt[e] = tt[e - 1];
+    if (lane == 0) {
+      tt[e] = tt[e - 1];
+      th[e] = th[e - 1];
+    }
     __syncwarp();
   }
   for (int i = lane; i < n; i += 32) tm[(uint64_t)ins * n + i] = pm[i];
   if (lane == 0) {
     tt[ins] = proposed;
+    th[ins] = h;
     if (!full) *tcount = count + 1;
   }
   __syncwarp();
 }
 
-__device__ __forceinline__ void tracker_offer_warp(uint64_t* tm, double* tt, int K, int n,
+__device__ __forceinline__ void tracker_offer_warp(uint64_t* tm, double* tt, uint64_t* th, int K, int n,
                                                    const uint64_t* pm, double proposed, int* tcount) {
   const int count = *tcount;
   if (count == K && proposed <= tt[count - 1]) return;  // full: not above the minimum
-  tracker_insert_warp(tm, tt, K, n, pm, proposed, tcount);
+  tracker_insert_warp(tm, tt, th, K, n, pm, proposed, tcount);
 }
 
 // Barrier over the TW warps of one team (a team runs one chain).
@@ -498,8 +514,6 @@ __global__ void __launch_bounds__(walk_cta_threads<TW>(), TW == 1 ? kWalkMinBloc
   if (c >= A.C) return;  // whole teams only: no later CTA-wide barrier when TW < 8
   TeamState& S = s_team[team];
   const bool score_only = A.perms != nullptr;
-  uint64_t* tm = score_only ? nullptr : A.tmasks + (uint64_t)c * A.K * n;
-  double* tt = score_only ? nullptr : A.ttotals + (uint64_t)c * A.K;
   if (ttid == 0) {
     if (score_only) {
       for (int i = 0; i < n; ++i) S.order[i] = (uint8_t)A.perms[(uint64_t)c * n + i];
@@ -663,7 +677,8 @@ __global__ void __launch_bounds__(walk_cta_threads<TW>(), TW == 1 ? kWalkMinBloc
     const bool accepted = S.accept;
     // ---- BestGraphTracker::update; every proposal is offered unless strict
     if (twarp == 0 && (t == 0 || accepted || !A.strict))
-      tracker_offer_warp(tm, tt, A.K, n, S.pm, proposed, &S.tcount);
+      tracker_offer_warp(A.tmasks + (uint64_t)c * A.K * n, A.ttotals + (uint64_t)c * A.K,
+                         A.thash + (uint64_t)c * A.K, A.K, n, S.pm, proposed, &S.tcount);
     // ---- commit + trace row
     if (accepted)
       for (int i = ttid; i < n; i += TW * 32) {
@@ -681,7 +696,7 @@ __global__ void __launch_bounds__(walk_cta_threads<TW>(), TW == 1 ? kWalkMinBloc
         const uint64_t o = (uint64_t)c * A.iters + (t - 1);
         A.tr_prop[o] = proposed;
         A.tr_acc[o] = accepted ? 1 : 0;
-        A.tr_best[o] = tt[0];
+        A.tr_best[o] = A.ttotals[(uint64_t)c * A.K];
       }
     }
     team_sync<TW>(team);
