@@ -186,6 +186,12 @@ int bnmc_gpu_last_scan_stats(const bnmc_table* t, uint64_t* row_rescans, uint64_
  * sorted walk, 1 full-row scan, 2 sorted walk). Results are identical. */
 int bnmc_gpu_table_set_scan_mode(bnmc_table* t, int mode);
 
+/* Sorted-walk tuning (results are identical for every setting): rows whose
+ * predecessor count p has S(p,s) <= enum_max are enumerated in PST order, the
+ * others walked (enum_max < 0: default 1024); ylists -1 auto / 0 off / 1 on
+ * selects the per-(row, node) lists used by delta walks. */
+int bnmc_gpu_table_set_walk_params(bnmc_table* t, int64_t enum_max, int ylists);
+
 /* Statistics of the last sorted-walk run_chains call: (chain, row) pairs
  * rescanned, sorted entries walked, PST entries enumerated (small predecessor
  * counts), and the device time of the last per-row sort build (ms). */

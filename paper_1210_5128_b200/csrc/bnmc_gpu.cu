@@ -161,6 +161,11 @@ struct bnmc_table {
   DevBuf<uint64_t> scm;
   DevBuf<double> eff;  // eff = ls + PpfTable::sum in global-index order
   uint64_t Sw = 0;     // sorted row stride
+  DevBuf<double> yeff;  // delta-walk lists [n][n-1][Syw]
+  DevBuf<uint64_t> ycm;
+  uint64_t Sy = 0, Syw = 0;
+  bool ylists = false;
+  int ylist_mode = -1;  // -1 auto (when they fit), 0 off, 1 on
   bool sorted_valid = false;
   float sort_ms = 0.f;
   DevBuf<uint64_t> pst;
@@ -168,6 +173,8 @@ struct bnmc_table {
   DevBuf<uint64_t> pst2;
   DevBuf<uint32_t> pst2_off;
   int pe = -1;
+  bool pst_ready = false;
+  uint64_t enum_max = kEnumMax;  // enumerate rows with S(p,s) <= enum_max, walk the others
   int scan_mode = 0;  // default for score_orders: 0 auto (walk), 1 full-row scan
   DevBuf<int> d_fo, d_tc;
   DevBuf<unsigned long long> d_acc;
@@ -416,6 +423,73 @@ TieCtx tie_ctx(const bnmc_table* t) {
 
 // eff = ls + PpfTable::sum in the scan's association (engine.cpp:50-51), fp64,
 // with each entry's candidate mask: the input of the per-row sort.
+// Delta-walk lists: for row v and candidate q, the entries of the sorted row
+// that contain q, in sorted order (ordered stream compaction, one CTA per
+// (q, v)), padded with never-admissible entries. Each list holds S(n-2, s-1)
+// entries; *err is set on a count mismatch.
+constexpr int kYThreads = 256, kYItems = 4;
+__global__ void __launch_bounds__(kYThreads) ylist_build_kernel(
+    const double* __restrict__ seff, const uint64_t* __restrict__ scm, uint64_t S, uint64_t Sw,
+    int n, double* yeff, uint64_t* ycm, uint64_t Sy, uint64_t Syw, int* err) {
+  const int q = blockIdx.x, v = blockIdx.y;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  __shared__ uint32_t s_warp[kYThreads / 32 + 1];
+  const double* re = seff + (uint64_t)v * Sw;
+  const uint64_t* rc = scm + (uint64_t)v * Sw;
+  const uint64_t lo = ((uint64_t)v * (n - 1) + q) * Syw;
+  double* oe = yeff + lo;
+  uint64_t* oc = ycm + lo;
+  const uint64_t bit = 1ull << q;
+  uint64_t out = 0;
+  for (uint64_t c0 = 0; c0 < S; c0 += (uint64_t)kYThreads * kYItems) {
+    double e[kYItems];
+    uint64_t m[kYItems];
+    uint32_t cnt = 0;
+#pragma unroll
+    for (int k = 0; k < kYItems; ++k) {
+      const uint64_t i = c0 + (uint64_t)tid * kYItems + k;
+      m[k] = i < S ? rc[i] : 0;
+      e[k] = i < S ? re[i] : 0.0;
+      cnt += (m[k] & bit) ? 1u : 0u;
+    }
+    // exclusive prefix of the per-thread counts over the CTA (warp scan + warp sums)
+    uint32_t incl = cnt;
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t x = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += x;
+    }
+    if (lane == 31) s_warp[warp] = incl;
+    __syncthreads();
+    if (tid == 0) {
+      uint32_t run = 0;
+      for (int w = 0; w < kYThreads / 32; ++w) {
+        const uint32_t t = s_warp[w];
+        s_warp[w] = run;
+        run += t;
+      }
+      s_warp[kYThreads / 32] = run;
+    }
+    __syncthreads();
+    uint64_t pos = out + s_warp[warp] + incl - cnt;
+#pragma unroll
+    for (int k = 0; k < kYItems; ++k)
+      if (m[k] & bit) {
+        if (pos < Sy) {
+          oe[pos] = e[k];
+          oc[pos] = m[k];
+        }
+        ++pos;
+      }
+    out += s_warp[kYThreads / 32];
+    __syncthreads();
+  }
+  if (tid == 0 && out != Sy) atomicExch(err, 6);
+  for (uint64_t i = Sy + tid; i < Syw; i += kYThreads) {
+    oe[i] = -INFINITY;
+    oc[i] = ~0ull;
+  }
+}
+
 // Padding of the sorted rows: eff -inf, mask ~0 (never admissible).
 __global__ void pad_sorted_kernel(double* seff, uint64_t* scm, uint64_t S, uint64_t Sw) {
   const uint64_t v = blockIdx.y;
@@ -471,7 +545,7 @@ void build_pst_table(int n, int s, int pmax, std::vector<uint64_t>& masks, std::
 // p < pe (the sets containing one given position, for delta rescans).
 void build_pst_small(bnmc_table* t) {
   int pe = -1;
-  for (int p = 0; p < t->n && bounded_count(p, t->s) <= kEnumMax; ++p) pe = p;
+  for (int p = 0; p < t->n && bounded_count(p, t->s) <= t->enum_max; ++p) pe = p;
   t->pe = pe;
   std::vector<uint64_t> m1, m2;
   std::vector<uint32_t> o1, o2;
@@ -492,7 +566,10 @@ void build_pst_small(bnmc_table* t) {
 // values keep ascending g). Rebuilt after every fold.
 void ensure_sorted(bnmc_table* t) {
   if (t->sorted_valid) return;
-  if (t->pe < 0 && t->pst_off.n == 0) build_pst_small(t);
+  if (!t->pst_ready) {
+    build_pst_small(t);
+    t->pst_ready = true;
+  }
   const uint64_t N = static_cast<uint64_t>(t->n) * t->S;
   // sorted rows padded with never-admissible entries so walk rounds need no
   // bounds checks: row stride Sw >= S + one full round
@@ -523,6 +600,26 @@ void ensure_sorted(bnmc_table* t) {
     CK(cub::DeviceRadixSort::SortPairsDescending(temp.p, temp_bytes, t->eff.p + o, t->seff.p + ow,
                                                  vals.p + o, t->scm.p + ow, static_cast<int>(t->S),
                                                  0, 64, t->stream));
+  }
+  // delta-walk lists, when they fit comfortably in device memory
+  t->Sy = t->s >= 1 && t->n >= 2 ? bounded_count(t->n - 2, t->s - 1) : 0;
+  t->Syw = (t->Sy + 32 * kWalkPadRound + 31) / 32 * 32;
+  const uint64_t ybytes = static_cast<uint64_t>(t->n) * (t->n - 1) * t->Syw * 16;
+  size_t free_b = 0, total_b = 0;
+  CK(cudaMemGetInfo(&free_b, &total_b));
+  const char* ydis = std::getenv("BNMC_NO_YLISTS");
+  t->ylists = t->Sy > 0 && !(ydis && ydis[0] == '1') && t->ylist_mode != 0 &&
+              (ybytes < free_b / 3 || t->ylist_mode == 1);
+  if (t->ylists) {
+    t->yeff.alloc(static_cast<size_t>(ybytes / 16));
+    t->ycm.alloc(static_cast<size_t>(ybytes / 16));
+    ylist_build_kernel<<<dim3(t->n - 1, t->n), kYThreads, 0, t->stream>>>(
+        t->seff.p, t->scm.p, t->S, t->Sw, t->n, t->yeff.p, t->ycm.p, t->Sy, t->Syw,
+        t->rowcnt.p + 2 * t->n + 1);
+    CK(cudaGetLastError());
+  } else {
+    t->yeff.release();
+    t->ycm.release();
   }
   CK(cudaEventRecord(e1, t->stream));
   CK(cudaEventSynchronize(e1));
@@ -563,6 +660,10 @@ WalkArgs walk_args(bnmc_table* t) {
   A.scm = t->scm.p;
   A.eff = t->eff.p;
   A.Sw = t->Sw;
+  A.yeff = t->ylists ? t->yeff.p : nullptr;
+  A.ycm = t->ylists ? t->ycm.p : nullptr;
+  A.Sy = t->Sy;
+  A.Syw = t->Syw;
   A.ls = t->ls.p;
   A.w = t->w.p;
   A.pst = t->pst.p;
@@ -1293,6 +1394,16 @@ int bnmc_gpu_table_set_scan_mode(bnmc_table* t, int mode) {
     if (!t) raise(BNMC_USAGE, "null table");
     if (mode < 0 || mode > 2) raise(BNMC_USAGE, "scan_mode must be 0, 1 or 2");
     t->scan_mode = mode;
+  });
+}
+
+int bnmc_gpu_table_set_walk_params(bnmc_table* t, int64_t enum_max, int ylists) {
+  return guarded([&] {
+    if (!t) raise(BNMC_USAGE, "null table");
+    t->enum_max = enum_max < 0 ? kEnumMax : static_cast<uint64_t>(enum_max);
+    t->pst_ready = false;
+    t->ylist_mode = ylists;
+    t->sorted_valid = false;
   });
 }
 

@@ -54,6 +54,9 @@ struct WalkArgs {
   const uint64_t* __restrict__ scm;   // [n][Sw] candidate masks in the same order
   const double* __restrict__ eff;     // [n][S] eff in global-index order
   uint64_t Sw;                        // sorted row stride (>= S + one walk round)
+  const double* __restrict__ yeff;    // [n][n-1][Syw] sorted entries of row v containing
+  const uint64_t* __restrict__ ycm;   //   candidate q (delta walks), or null
+  uint64_t Sy, Syw;                   // entries per list, padded stride
   const double* __restrict__ ls;      // [n][S] local scores, BNSC order
   const double* __restrict__ w;       // [n][n] PPF weights
   const uint64_t* __restrict__ pst;   // position masks of PST(p) for p <= pe, concatenated
@@ -158,7 +161,8 @@ struct WalkHit {
 // advances base; true once the first admissible entry is found.
 template <int U>
 __device__ __forceinline__ bool walk_round(const double* re, const uint64_t* rc, uint64_t ncp,
-                                           uint64_t S, uint64_t& base, int lane, WalkHit& h) {
+                                           uint64_t S, uint64_t& base, int lane, WalkHit& h,
+                                           double floor = -INFINITY, bool* exhausted = nullptr) {
   if (base >= S) return false;
   double e[U];
   uint64_t c[U];
@@ -168,20 +172,25 @@ __device__ __forceinline__ bool walk_round(const double* re, const uint64_t* rc,
     e[u] = __ldg(re + i);
     c[u] = __ldg(rc + i);
   }
-  // first group holding an admissible entry; its values selected without
-  // dynamic register indexing, then one set of shuffles
+  // first group holding an admissible entry (at or above `floor`); its values
+  // selected without dynamic register indexing, then one set of shuffles
   int hu = -1;
   unsigned hb = 0;
 #pragma unroll
   for (int u = U - 1; u >= 0; --u) {
-    const unsigned bal = __ballot_sync(0xffffffffu, (c[u] & ncp) == 0);
+    const unsigned bal = __ballot_sync(0xffffffffu, (c[u] & ncp) == 0 && e[u] >= floor);
     if (bal) {
       hu = u;
       hb = bal;
     }
   }
   base += 32 * U;
-  if (hu < 0) return false;
+  if (hu < 0) {
+    // sorted descending: once the round's last entry is below the floor, no
+    // later entry can qualify
+    if (exhausted && __shfl_sync(0xffffffffu, e[U - 1], 31) < floor) *exhausted = true;
+    return false;
+  }
   double eh = e[0], en = U > 1 ? e[1 < U ? 1 : 0] : e[0];
   uint64_t ch = c[0];
 #pragma unroll
@@ -310,6 +319,7 @@ __device__ __forceinline__ PairOut enum_pst(const WalkArgs& A, int v, const uint
 struct DeltaIn {
   bool on;
   int ypos;        // position of Y in the proposed order
+  int ynode;       // Y
   double old_eff;
   uint64_t old_cm;  // candidate mask of the current best
 };
@@ -343,10 +353,43 @@ __device__ PairOut pair_argmax(const WalkArgs& A, int v, int p, uint64_t cpred, 
     }
     return r;
   }
+  const uint64_t ncp = ~cpred;
+  if (d.on && A.yeff) {
+    // ---- delta walk: only sets containing Y can beat the current best, so
+    // walk row v's list of entries containing Y down to the current best's
+    // value (SURVEY §7 "incremental middle rows")
+    const int qy = d.ynode - (d.ynode > v);
+    const uint64_t lo = ((uint64_t)v * (A.n - 1) + qy) * A.Syw;
+    const double* ye = A.yeff + lo;
+    const uint64_t* yc = A.ycm + lo;
+    WalkHit h;
+    bool done = false;
+    uint64_t base = 0;
+    if (!walk_round<1>(ye, yc, ncp, A.Sy, base, lane, h, d.old_eff, &done) && !done &&
+        !walk_round<2>(ye, yc, ncp, A.Sy, base, lane, h, d.old_eff, &done) && !done)
+      while (base < A.Sy && !done && !walk_round<WU>(ye, yc, ncp, A.Sy, base, lane, h, d.old_eff, &done)) {
+      }
+    if (lane == 0) *walked += base;
+    r.eff = d.old_eff;
+    r.cm = d.old_cm;
+    r.tied = 0;
+    if (h.start == ~0ull) return r;  // no set containing Y reaches the current best
+    int ties = 0;
+    uint64_t cm = h.kcm;
+    if (!h.next_differs) cm = collect_ties(ye, yc, ncp, A.Sy, h.start, h.kstar, h.kcm, v, ppos, &ties);
+    if (h.kstar > d.old_eff) {
+      r.eff = h.kstar;
+      r.cm = cm;
+      r.tied = ties > 0;
+    } else {  // equal to the current best: an exact tie, position rule decides
+      r.tied = 1;
+      if (!prefer_pos(d.old_cm, cm, v, ppos)) r.cm = cm;
+    }
+    return r;
+  }
   // ---- walk of the sorted row
   const double* re = A.seff + (uint64_t)v * A.Sw;
   const uint64_t* rc = A.scm + (uint64_t)v * A.Sw;
-  const uint64_t ncp = ~cpred;
   const uint64_t S = A.S;
   WalkHit h;
   // Rounds grow 32, 64, 128, then 256 entries: most first admissible entries
@@ -614,7 +657,7 @@ __global__ void __launch_bounds__(walk_cta_threads<TW>(), TW == 1 ? kWalkMinBloc
         // middle rows of a swap: the node at hi (X) left the predecessors, the
         // node at lo (Y) joined; eligible when the current best avoids X and
         // is not an exact tie
-        S.pd[slot] = (uint8_t)(t > 0 && p > lo && p < hi && p <= A.pe &&
+        S.pd[slot] = (uint8_t)(t > 0 && p > lo && p < hi && (p <= A.pe || A.yeff) &&
                                !((S.tied >> v) & 1ull) && !((S.cm[v] >> S.prop[hi]) & 1ull));
         ++slot;
       }
@@ -628,6 +671,7 @@ __global__ void __launch_bounds__(walk_cta_threads<TW>(), TW == 1 ? kWalkMinBloc
       DeltaIn d;
       d.on = S.pd[q] != 0;
       d.ypos = lo;
+      d.ynode = S.prop[lo];
       d.old_eff = S.cb[v];
       d.old_cm = nodes_to_cand(S.cm[v], v);
       // few chains in flight (TW >= 8): more independent gathers per lane

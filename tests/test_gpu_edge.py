@@ -286,3 +286,30 @@ def test_device_acceptance_and_exact_replay():
             np.testing.assert_array_equal(getattr(b, f), getattr(ref_b, f), err_msg=f)
     o = port.run_mcmc(cache.table(), 4, 150, seeds[7], pri)
     np.testing.assert_array_equal(ref_b.trace_proposed[7], o["trace_proposed"])
+
+
+@pytest.mark.parametrize("enum_max,ylists", [(0, 1), (0, 0), (-1, 1), (1 << 40, 0)])
+def test_walk_tuning_paths_identical(enum_max, ylists):
+    """Every walk-path variant — all rows walked (with / without the delta-walk
+    lists), default split, all rows enumerated — on tie-heavy and ordinary
+    instances gives the oracle's chains and order scores bit for bit."""
+    import ctypes as C
+    for cells, cards, s, gamma in (rand_instance(21, 14, 3, cmax=2) + (3, 1.0),
+                                   rand_instance(23, 16, 400) + (3, 0.2)):
+        cfg = P.RunConfig(max_parents=s, gamma=gamma, iterations=200, scan_mode=2)
+        cache = P.ScoreCache.build(P.Dataset(cards, cells), cfg)
+        _lib.check(_lib.lib().bnmc_gpu_table_set_walk_params(cache.handle, enum_max, ylists))
+        t = port.cache_build(cells, cards, s, gamma, 1.0)
+        rs = P.run_chains(cache, None, [1, 2, 3], cfg)
+        for c, seed in enumerate([1, 2, 3]):
+            o = port.run_mcmc(t, s, 200, seed)
+            np.testing.assert_array_equal(rs[c].trace_proposed, o["trace_proposed"])
+            np.testing.assert_array_equal(rs[c].tracker_masks, o["tracker_masks"])
+            np.testing.assert_array_equal(rs[c].final_order, o["final_order"])
+        perms = np.stack([np.random.default_rng(i).permutation(cells.shape[1])
+                          for i in range(6)]).astype(np.int32)
+        masks, best, tot = P.OrderScorer(cache, None, scan_mode=2).score_many(perms)
+        for i in range(6):
+            om, ob, ot = port.score_order(t, s, perms[i])
+            np.testing.assert_array_equal(masks[i], om)
+            assert tot[i] == ot
