@@ -39,7 +39,10 @@ namespace bnmc_dev {
 
 constexpr int kHMax = 4096;   // max joint cells of a set U (dense counter bound)
 constexpr int kRPMax = 1024;  // max configurations of a prefix P
-constexpr int kK1Threads = 256;
+#ifndef BNMC_K1_THREADS
+#define BNMC_K1_THREADS 256
+#endif
+constexpr int kK1Threads = BNMC_K1_THREADS;
 constexpr int kMaxPrefix = 8;  // members of a prefix P (|P| <= s <= 8)
 
 struct K1Args {

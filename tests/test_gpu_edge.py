@@ -313,3 +313,36 @@ def test_walk_tuning_paths_identical(enum_max, ylists):
             om, ob, ot = port.score_order(t, s, perms[i])
             np.testing.assert_array_equal(masks[i], om)
             assert tot[i] == ot
+
+
+def test_randomized_instances_all_paths():
+    """Property test over random instances (sizes, cardinalities, s, gamma, ess,
+    K2, priors incl. extremes, tiny and empty samples): device table, order
+    scores and chains on both scan paths equal the oracle's bit for bit."""
+    rng = np.random.default_rng(2024)
+    for trial in range(14):
+        n = int(rng.integers(2, 23))
+        s = int(rng.integers(0, 6))
+        m = int(rng.choice([0, 1, 7, 60, 400]))
+        cells, cards = rand_instance(1000 + trial, n, m, cmax=int(rng.integers(2, 5)))
+        gamma, ess, k2 = float(rng.choice([0.1, 0.5, 1.0])), float(rng.choice([1.0, 3.0])), bool(trial % 3 == 0)
+        pri = np.where(rng.random((n, n)) < 0.3, rng.choice([0.0, 0.1, 0.9, 1.0], (n, n)), 0.5)
+        cfg = P.RunConfig(max_parents=s, gamma=gamma, ess=ess,
+                          alpha_mode=P.AlphaMode.K2 if k2 else P.AlphaMode.BDEU, iterations=60)
+        cache = P.ScoreCache.build(P.Dataset(cards, cells), cfg)
+        t = port.cache_build(cells, cards, s, gamma, ess, k2=k2)
+        np.testing.assert_array_equal(cache.table().view(np.uint64), t.view(np.uint64))
+        perms = np.stack([rng.permutation(n) for _ in range(4)]).astype(np.int32)
+        for mode in (1, 2):
+            masks, best, tot = P.OrderScorer(cache, pri, scan_mode=mode).score_many(perms)
+            for i in range(4):
+                om, ob, ot = port.score_order(t, s, perms[i], pri)
+                np.testing.assert_array_equal(masks[i], om)
+                assert tot[i] == ot
+            if n >= 2 and m > 0:
+                cfg.scan_mode = mode
+                rs = P.run_chains(cache, pri, [trial + 1, trial + 50], cfg)
+                for c, seed in enumerate([trial + 1, trial + 50]):
+                    o = port.run_mcmc(t, s, 60, seed, pri)
+                    np.testing.assert_array_equal(rs[c].trace_proposed, o["trace_proposed"])
+                    np.testing.assert_array_equal(rs[c].tracker_masks, o["tracker_masks"])
