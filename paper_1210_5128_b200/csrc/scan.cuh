@@ -126,20 +126,23 @@ struct ScanArgs {
 // CTA, one pair of global atomics per CTA and pair — the same (key, g) /
 // (key, ~g) cells and exact tie resolution in K3 as the v1 kernel.
 constexpr int kScan2Threads = 256;
-constexpr int kScan2Per = 8;         // entries (one 32-B key sector) per thread
-constexpr int kScan2Rows = 2;        // rows in flight per pass
+#ifndef BNMC_SCAN2_PER
+#define BNMC_SCAN2_PER 8
+#endif
+constexpr int kScan2Per = BNMC_SCAN2_PER;  // entries (32-B key sectors x 8) per thread
 constexpr int kScan2RowGroups = 8;   // gridDim.y: CTA (x, y) takes rows y, y + 8, ... of the step
+constexpr int kScan2MaxRows = (kMaxNodes + kScan2RowGroups - 1) / kScan2RowGroups;
 
-__global__ void __launch_bounds__(kScan2Threads, 4) scan2_kernel(ScanArgs a) {
+__global__ void __launch_bounds__(kScan2Threads, kScan2Per > 8 ? 2 : 4) scan2_kernel(ScanArgs a) {
   __shared__ int s_cnt[64], s_rows[64], s_nrows, s_sel;
   __shared__ uint64_t s_union[64];
-  __shared__ unsigned long long s_cell[kScan2Rows][kMaxChains][2];
+  __shared__ unsigned long long s_cell[kScan2MaxRows][kMaxChains][2];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int n = a.n;
-  const uint64_t slot = (uint64_t)blockIdx.x * kScan2Threads + tid;  // 16-B key slot
+  const uint64_t slot = (uint64_t)blockIdx.x * kScan2Threads + tid;
   const bool mine_ok = slot * kScan2Per < (uint64_t)a.sectors * 8;
   const uint64_t g0 = slot * kScan2Per;
-  // ---- prologue (independent of the previous kernel): masks of my entries
+  // ---- prologue (independent of the previous kernel): masks of my sector
   uint64_t m[kScan2Per];
   uint64_t inter = ~0ull;
   {
@@ -153,7 +156,7 @@ __global__ void __launch_bounds__(kScan2Threads, 4) scan2_kernel(ScanArgs a) {
 #pragma unroll
     for (int e = 0; e < kScan2Per; ++e) inter &= m[e];
   }
-  for (int i = tid; i < kScan2Rows * kMaxChains * 2; i += kScan2Threads) (&s_cell[0][0][0])[i] = 0ull;
+  for (int i = tid; i < kScan2MaxRows * kMaxChains * 2; i += kScan2Threads) (&s_cell[0][0][0])[i] = 0ull;
   cudaGridDependencySynchronize();
   if (tid == 0) s_sel = *a.sel;
   __syncthreads();
@@ -185,92 +188,87 @@ __global__ void __launch_bounds__(kScan2Threads, 4) scan2_kernel(ScanArgs a) {
     if (lane == 0) s_union[v] = u;
   }
   __syncthreads();
+  // ---- rows of this CTA, no barriers: the next row's keys are in flight
+  // while the current row's pairs are reduced into shared cells
   unsigned long long loads = 0;
-  for (int r0 = 0; r0 < myrows; r0 += kScan2Rows) {
-    float k[kScan2Rows][kScan2Per];
-    bool have[kScan2Rows];
+  float kn[kScan2Per];
+  bool hn = false;
+  auto fetch = [&](int i, float* k) -> bool {
+    if (i >= myrows || !mine_ok) return false;
+    const int v = s_rows[ry + i * RG];
+    if ((inter & ~s_union[v]) != 0) return false;  // no entry admissible for any pair
+    const float4* src = reinterpret_cast<const float4*>(a.keys + (uint64_t)v * a.Sp + g0);
 #pragma unroll
-    for (int j = 0; j < kScan2Rows; ++j) {
-      have[j] = false;
-      if (r0 + j < myrows && mine_ok) {
-        const int v = s_rows[ry + (r0 + j) * RG];
-        have[j] = (inter & ~s_union[v]) == 0;
-        if (have[j]) {
-          const float4* src = reinterpret_cast<const float4*>(a.keys + (uint64_t)v * a.Sp + g0);
-#pragma unroll
-          for (int h = 0; h < kScan2Per / 4; ++h) {
-            const float4 x = __ldcs(src + h);  // streamed once per launch
-            k[j][4 * h] = x.x;
-            k[j][4 * h + 1] = x.y;
-            k[j][4 * h + 2] = x.z;
-            k[j][4 * h + 3] = x.w;
-          }
-          loads += kScan2Per / 4;
-        }
-      }
+    for (int h = 0; h < kScan2Per / 4; ++h) {
+      const float4 x = __ldcs(src + h);  // streamed once per launch
+      k[4 * h] = x.x;
+      k[4 * h + 1] = x.y;
+      k[4 * h + 2] = x.z;
+      k[4 * h + 3] = x.w;
     }
+    loads += kScan2Per / 4;
+    return true;
+  };
+  hn = fetch(0, kn);
+  for (int i = 0; i < myrows; ++i) {
+    float k[kScan2Per];
 #pragma unroll
-    for (int j = 0; j < kScan2Rows; ++j) {
-      if (r0 + j >= myrows) break;
-      const int v = s_rows[ry + (r0 + j) * RG];
-      const int cnt = s_cnt[v];
-      for (int q = 0; q < cnt; ++q) {
-        const uint64_t ncp = ~a.buckets[(b * n + v) * kMaxChains + q].cpred;
-        float mx = -INFINITY;
-        int ge = -1;
-        bool tie = false;
-        if (have[j]) {
+    for (int e = 0; e < kScan2Per; ++e) k[e] = kn[e];
+    const bool have = hn;
+    hn = fetch(i + 1, kn);
+    const int v = s_rows[ry + i * RG];
+    const int cnt = s_cnt[v];
+    for (int q = 0; q < cnt; ++q) {
+      const uint64_t ncp = ~a.buckets[(b * n + v) * kMaxChains + q].cpred;
+      float mx = -INFINITY;
+      int ge = -1;
+      bool tie = false;
+      if (have) {
 #pragma unroll
-          for (int e = 0; e < kScan2Per; ++e) {
-            if ((m[e] & ncp) == 0) {
-              if (k[j][e] > mx) {
-                mx = k[j][e];
-                ge = e;
-                tie = false;
-              } else if (k[j][e] == mx) {
-                tie = true;
-              }
+        for (int e = 0; e < kScan2Per; ++e) {
+          if ((m[e] & ncp) == 0) {
+            if (k[e] > mx) {
+              mx = k[e];
+              ge = e;
+              tie = false;
+            } else if (k[e] == mx) {
+              tie = true;
             }
           }
         }
-        const uint32_t ko = ge >= 0 ? ordkey(mx) : 0u;
-        const uint32_t mxw = __reduce_max_sync(0xffffffffu, ko);
-        if (mxw != 0u) {
-          const bool win = ko == mxw;
-          const uint32_t g = (uint32_t)(g0 + (ge < 0 ? 0 : ge));
-          const uint32_t ghi = __reduce_max_sync(0xffffffffu, win ? g : 0u);
-          // a lane-level tie forces glo != ghi so the step kernel resolves it
-          const uint32_t mn = win ? (tie ? (g == 0 ? 1u : g - 1u) : g) : 0xFFFFFFFFu;
-          const uint32_t glo = __reduce_min_sync(0xffffffffu, mn);
-          if (lane == 0) {
-            atomicMax(&s_cell[j][q][0], ((unsigned long long)mxw << 32) | ghi);
-            atomicMax(&s_cell[j][q][1], ((unsigned long long)mxw << 32) | (uint32_t)~glo);
-          }
+      }
+      const uint32_t ko = ge >= 0 ? ordkey(mx) : 0u;
+      const uint32_t mxw = __reduce_max_sync(0xffffffffu, ko);
+      if (mxw != 0u) {
+        const bool win = ko == mxw;
+        const uint32_t g = (uint32_t)(g0 + (ge < 0 ? 0 : ge));
+        const uint32_t ghi = __reduce_max_sync(0xffffffffu, win ? g : 0u);
+        // a lane-level tie forces glo != ghi so the step kernel resolves it
+        const uint32_t mn = win ? (tie ? (g == 0 ? 1u : g - 1u) : g) : 0xFFFFFFFFu;
+        const uint32_t glo = __reduce_min_sync(0xffffffffu, mn);
+        if (lane == 0) {
+          atomicMax(&s_cell[i][q][0], ((unsigned long long)mxw << 32) | ghi);
+          atomicMax(&s_cell[i][q][1], ((unsigned long long)mxw << 32) | (uint32_t)~glo);
         }
       }
     }
-    __syncthreads();
-    // flush the CTA's maxima of these rows' pairs to the global cells
-#pragma unroll
-    for (int j = 0; j < kScan2Rows; ++j) {
-      if (r0 + j >= myrows) break;
-      const int v = s_rows[ry + (r0 + j) * RG];
-      const int cnt = s_cnt[v];
-      for (int q = tid; q < cnt; q += kScan2Threads) {
-        const unsigned long long c0 = s_cell[j][q][0], c1 = s_cell[j][q][1];
-        if (c0 != 0ull) {
-          const PairRec pr = a.buckets[(b * n + v) * kMaxChains + q];
-          unsigned long long* cell = a.cell + 2ull * (pr.chain * n + pr.slot);
-          atomicMax(cell, c0);
-          atomicMax(cell + 1, c1);
-          s_cell[j][q][0] = 0ull;
-          s_cell[j][q][1] = 0ull;
-        }
-      }
-    }
-    __syncthreads();
   }
-  if (a.sector_loads) {  // 16-byte slots loaded, reported in 32-byte sectors
+  __syncthreads();
+  // ---- the CTA's maxima of its rows' pairs into the global cells
+  for (int i = 0; i < myrows; ++i) {
+    const int v = s_rows[ry + i * RG];
+    const int cnt = s_cnt[v];
+    for (int q = tid; q < cnt; q += kScan2Threads) {
+      const unsigned long long c0 = s_cell[i][q][0], c1 = s_cell[i][q][1];
+      if (c0 != 0ull) {
+        const PairRec pr = a.buckets[(b * n + v) * kMaxChains + q];
+        unsigned long long* cell = a.cell + 2ull * (pr.chain * n + pr.slot);
+        atomicMax(cell, c0);
+        atomicMax(cell + 1, c1);
+      }
+    }
+  }
+  if (a.sector_loads) {  // 16-byte key slots loaded
     for (int off = 16; off > 0; off >>= 1) loads += __shfl_down_sync(0xffffffffu, loads, off);
     if (lane == 0 && loads) atomicAdd(a.sector_loads, loads);
   }
