@@ -188,7 +188,7 @@ int bnmc_gpu_table_set_scan_mode(bnmc_table* t, int mode);
 
 /* Sorted-walk tuning (results are identical for every setting): rows whose
  * predecessor count p has S(p,s) <= enum_max are enumerated in PST order, the
- * others walked (enum_max < 0: default 1024); ylists -1 auto / 0 off / 1 on
+ * others walked (enum_max < 0: default 64); ylists -1 auto / 0 off / 1 on
  * selects the per-(row, node) lists used by delta walks. */
 int bnmc_gpu_table_set_walk_params(bnmc_table* t, int64_t enum_max, int ylists);
 

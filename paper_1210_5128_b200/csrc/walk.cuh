@@ -47,7 +47,7 @@ constexpr int kWalkMinBlocks1 = BNMC_WALK_MINB1;  // CTAs per SM targeted for on
 #define BNMC_ENUM_UNROLL 1
 #endif
 constexpr int kEnumUnroll = BNMC_ENUM_UNROLL;  // independent gathers per lane per enumeration step
-constexpr uint64_t kEnumMax = 1024;        // enumerate when S(p,s) <= this
+constexpr uint64_t kEnumMax = 64;          // enumerate when S(p,s) <= this (walk above)
 
 struct WalkArgs {
   const double* __restrict__ seff;    // [n][Sw] eff, sorted descending per row, padded

@@ -18,6 +18,8 @@ t0 = time.perf_counter()
 cache = P.ScoreCache.build(data, cfg, pri)
 print(f"build {time.perf_counter() - t0:.3f}s", flush=True)
 cfg.iterations = iters
+if os.environ.get("BNMC_ENUM_MAX"):
+    _lib.check(_lib.lib().bnmc_gpu_table_set_walk_params(cache.handle, int(os.environ["BNMC_ENUM_MAX"]), -1))
 tws = [int(x) for x in os.environ.get("TW", "0").split(",")]
 for tw in tws:
     mode = 2
