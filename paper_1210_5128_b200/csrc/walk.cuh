@@ -32,6 +32,9 @@
 
 namespace bnmc_dev {
 
+#ifndef BNMC_WALK_ROUND_INLINE
+#define BNMC_WALK_ROUND_INLINE __forceinline__
+#endif
 constexpr int kWalkThreads = 256;
 constexpr int kWalkWarps = kWalkThreads / 32;
 #ifndef BNMC_WALK_UNROLL
@@ -160,7 +163,7 @@ struct WalkHit {
 // One walk round of U entries per lane at sorted indices [base, base + 32U);
 // advances base; true once the first admissible entry is found.
 template <int U>
-__device__ __forceinline__ bool walk_round(const double* re, const uint64_t* rc, uint64_t ncp,
+__device__ BNMC_WALK_ROUND_INLINE bool walk_round(const double* re, const uint64_t* rc, uint64_t ncp,
                                            uint64_t S, uint64_t& base, int lane, WalkHit& h,
                                            double floor = -INFINITY, bool* exhausted = nullptr) {
   if (base >= S) return false;
