@@ -7,6 +7,8 @@
 //   test_dropin cpu   host-only cases (no device calls)
 //   test_dropin gpu   every case (needs a B200)
 #include <algorithm>
+#include <filesystem>
+#include <fstream>
 #include <cmath>
 #include <cstdio>
 #include <map>
@@ -17,6 +19,7 @@
 #include "../../include/bnmc_synth.h"
 #include "../../oracle/bnmc_oracle.h"
 #include "bnmc/engine.hpp"
+#include "bnmc/io.hpp"
 #include "bnmc/sampler.hpp"
 #include "bnmc/scoring.hpp"
 #include "mini_test.hpp"
@@ -156,6 +159,50 @@ TEST_CASE("value types validate like the reference", false) {
   CHECK_THROWS_AS(cfg.validate(), UsageError);
   CHECK(ScoreCache::estimate_bytes(60, 4) == 60ull * 489406ull * 8ull);
   CHECK_THROWS_AS(ScoreCache().device_table(), UsageError);
+}
+
+
+TEST_CASE("io: dataset / prior / edge-list round trips and errors", false) {  // test_io.cpp
+  const std::string dir = "/tmp/bnmc_dropin_io";
+  std::filesystem::create_directories(dir);
+  const Dataset d({2, 3, 4}, {0, 1, 2, 1, 2, 3, 0, 0, 1});
+  write_dataset_csv(dir + "/d.csv", d);
+  CHECK(read_dataset_csv(dir + "/d.csv") == d);
+  {  // cardinalities inferred without "#cards:" (max state + 1, floor 2)
+    std::ofstream f(dir + "/e.csv");
+    f << "a,b\n0,0\n\n1,0\r\n# comment\n";
+  }
+  const Dataset e = read_dataset_csv(dir + "/e.csv");
+  CHECK(e.rows() == 2);
+  CHECK(e.cardinality(0) == 2);
+  CHECK(e.cardinality(1) == 2);
+  {
+    std::ofstream f(dir + "/bad.csv");
+    f << "a,b\n0,1,2\n";
+  }
+  CHECK_THROWS_AS(read_dataset_csv(dir + "/bad.csv"), DataError);
+  CHECK_THROWS_AS(read_dataset_csv(dir + "/missing.csv"), DataError);
+  PriorMatrix pr = PriorMatrix::neutral(3);
+  pr.set(0, 2, 0.75);
+  pr.set(2, 1, 0.125);
+  write_prior_csv(dir + "/p.csv", pr);
+  const PriorMatrix back = read_prior_csv(dir + "/p.csv", 3);
+  CHECK(back.r(0, 2) == 0.75);
+  CHECK(back.r(2, 1) == 0.125);
+  CHECK_THROWS_AS(read_prior_csv(dir + "/p.csv", 4), DataError);
+  Dag g(5);
+  g.add_edge(0, 3);
+  g.add_edge(4, 3);
+  g.add_edge(1, 2);
+  write_edge_list(dir + "/g.edges", g);
+  CHECK(read_edge_list(dir + "/g.edges") == g);  // "# nodes:" keeps isolated nodes
+  CHECK(read_edge_list(dir + "/g.edges").n() == 5);
+  CHECK(format_double(0.1) == "0.1");
+  CHECK(format_double(-4251.749719875) == "-4251.749719875");
+  const ConfusionCounts c = confusion(g, Dag(5));
+  CHECK(c.fp == 3);
+  CHECK(c.tn == 17);
+  CHECK(c.f1() == 0.0);
 }
 
 // ------------------------------------------------------------- device
