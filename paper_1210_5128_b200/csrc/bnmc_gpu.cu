@@ -217,7 +217,7 @@ namespace {
 constexpr int kMaxChainsPerLaunch = 64;
 
 struct ScanGeom {
-  int G, Ls, RB, sectors;
+  int G, sectors;
 };
 
 // CTA b owns Ls <= 512 consecutive sectors of every row (one CTA per SM when
@@ -226,8 +226,6 @@ ScanGeom scan_geometry(const bnmc_table* t, int max_pairs) {
   ScanGeom g;
   (void)max_pairs;
   g.sectors = static_cast<int>(t->Sp / 8);
-  g.Ls = 0;
-  g.RB = 0;
   const uint64_t slots = (static_cast<uint64_t>(g.sectors) * 8 + kScan2Per - 1) / kScan2Per;
   g.G = static_cast<int>((slots + kScan2Threads - 1) / kScan2Threads);
   return g;
@@ -236,7 +234,7 @@ ScanGeom scan_geometry(const bnmc_table* t, int max_pairs) {
 // K2 (scan2_kernel): one thread per 32-byte key sector of every row.
 void launch_scan(const ScanGeom& g, ScanArgs a, int max_pairs, cudaStream_t s, bool pdl) {
   a.sectors = g.sectors;
-  a.max_pairs = max_pairs;
+  (void)max_pairs;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(g.G, kScan2RowGroups);
   cfg.blockDim = dim3(kScan2Threads);
@@ -748,11 +746,8 @@ ScanArgs scan_args(const bnmc_table* t, const ScanGeom& g) {
   sa.cell = t->cell.p;
   sa.n = t->n;
   sa.sectors = g.sectors;
-  sa.Ls = g.Ls;
-  sa.RB = g.RB;
   sa.tie = tie_ctx(t);
   sa.sector_loads = t->stat.p + 1;
-  if (const char* e = std::getenv("BNMC_DEBUG_SCAN_EXIT")) sa.debug_exit = std::atoi(e);
   return sa;
 }
 

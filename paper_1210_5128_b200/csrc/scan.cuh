@@ -104,13 +104,9 @@ struct ScanArgs {
   const uint8_t* ppos;      // [C][64] positions of the proposed order
   unsigned long long* cell; // [C][n][2] packed maxima (key,g) / (key,~g)
   int n;
-  int max_pairs;            // C * n (capacity of the shared pair list)
   int sectors;              // Sp / 8
-  int Ls;                   // sectors per CTA
-  int RB;                   // rows per pipeline stage
   TieCtx tie;
   unsigned long long* sector_loads;  // optional: sectors streamed (statistics)
-  int debug_exit;                    // development: stop after phase k (0 = full)
 };
 
 // ---------------------------------------------------------------------------
