@@ -271,7 +271,7 @@ def run_ours(args):
             "metric": METRIC, "value": value, "unit": "iterations/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": tot_dev * 1e3 / args.steps, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64 (exact scores) + u64 parent masks",
+            "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (reference generator, seed 7, SURVEY \u00a78d)",
             "config": {"workload": f"{args.config}: n=60 k=4 m=10000 3-state + pairwise priors; "
                                    f"{Cn} independent chains/GPU x {I} iterations per step",
