@@ -639,6 +639,17 @@ void launch_walk(bnmc_table* t, const WalkArgs& A, int C, int team_warps = 0) {
   const int cta = std::max(kWalkThreads, 32 * tw);
   const int per = cta / (32 * tw);
   const unsigned grid = static_cast<unsigned>((C + per - 1) / per);
+  static const bool no_spec = [] {
+    const char* e = std::getenv("BNMC_NO_SPEC");
+    return e && e[0] == '1';
+  }();
+  if (tw == 32 && A.perms == nullptr && !no_spec) {
+    // few chains: one 1024-thread CTA per chain evaluating kSpecD proposals per round
+    walk_spec_kernel<<<C, 1024, 0, t->stream>>>(A);
+    CK(cudaGetLastError());
+    t->last_team = 32;
+    return;
+  }
   switch (tw) {
     case 32: walk_chain_kernel<32><<<grid, cta, 0, t->stream>>>(A); break;
     case 16: walk_chain_kernel<16><<<grid, cta, 0, t->stream>>>(A); break;

@@ -433,7 +433,8 @@ __device__ PairOut pair_argmax(const WalkArgs& A, int v, int p, uint64_t cpred, 
 // graph equality, reject when full and total <= the minimum, insert at the
 // lower bound of (total desc, Dag operator< over the parent masks).
 __device__ __noinline__ void tracker_insert_warp(uint64_t* tm, double* tt, uint64_t* th, int K, int n,
-                                                 const uint64_t* pm, double proposed, int* tcount) {
+                                                 const uint64_t* pm, double proposed, int* tcount,
+                                                 double* tcache) {
   const int lane = threadIdx.x & 31;
   const int count = *tcount;
   const bool full = count == K;
@@ -486,16 +487,21 @@ __device__ __noinline__ void tracker_insert_warp(uint64_t* tm, double* tt, uint6
   if (lane == 0) {
     tt[ins] = proposed;
     th[ins] = h;
-    if (!full) *tcount = count + 1;
+    const int cnt = full ? count : count + 1;
+    *tcount = cnt;
+    tcache[0] = tt[0];                                // best (trace rows)
+    tcache[1] = cnt == K ? tt[K - 1] : -INFINITY;     // admission threshold when full
   }
   __syncwarp();
 }
 
+// tcache (shared): [0] tracker best, [1] minimum when full (else -inf), kept
+// current by the insert so the common rejection needs no global load.
 __device__ __forceinline__ void tracker_offer_warp(uint64_t* tm, double* tt, uint64_t* th, int K, int n,
-                                                   const uint64_t* pm, double proposed, int* tcount) {
-  const int count = *tcount;
-  if (count == K && proposed <= tt[count - 1]) return;  // full: not above the minimum
-  tracker_insert_warp(tm, tt, th, K, n, pm, proposed, tcount);
+                                                   const uint64_t* pm, double proposed, int* tcount,
+                                                   double* tcache) {
+  if (proposed <= tcache[1]) return;  // full: not above the minimum
+  tracker_insert_warp(tm, tt, th, K, n, pm, proposed, tcount, tcache);
 }
 
 // Barrier over the TW warps of one team (a team runs one chain).
@@ -523,6 +529,7 @@ struct TeamState {
   double cb[64];                   // current per-node bests
   uint64_t tied, tied_new, rng, arng;
   double total, cur_total;
+  double tcache[2];                // tracker best, admission threshold
   unsigned long long acc;
   int np, a, b, accept, tcount, amb;
 };
@@ -580,6 +587,8 @@ __global__ void __launch_bounds__(walk_cta_threads<TW>(), TW == 1 ? kWalkMinBloc
     S.tied = 0;
     S.amb = 0;
     S.tcount = 0;
+    S.tcache[0] = -INFINITY;
+    S.tcache[1] = -INFINITY;
     S.acc = 0;
     S.cur_total = 0.0;
   }
@@ -725,7 +734,7 @@ __global__ void __launch_bounds__(walk_cta_threads<TW>(), TW == 1 ? kWalkMinBloc
     // ---- BestGraphTracker::update; every proposal is offered unless strict
     if (twarp == 0 && (t == 0 || accepted || !A.strict))
       tracker_offer_warp(A.tmasks + (uint64_t)c * A.K * n, A.ttotals + (uint64_t)c * A.K,
-                         A.thash + (uint64_t)c * A.K, A.K, n, S.pm, proposed, &S.tcount);
+                         A.thash + (uint64_t)c * A.K, A.K, n, S.pm, proposed, &S.tcount, S.tcache);
     // ---- commit + trace row
     if (accepted)
       for (int i = ttid; i < n; i += TW * 32) {
@@ -743,7 +752,7 @@ __global__ void __launch_bounds__(walk_cta_threads<TW>(), TW == 1 ? kWalkMinBloc
         const uint64_t o = (uint64_t)c * A.iters + (t - 1);
         A.tr_prop[o] = proposed;
         A.tr_acc[o] = accepted ? 1 : 0;
-        A.tr_best[o] = A.ttotals[(uint64_t)c * A.K];
+        A.tr_best[o] = S.tcache[0];
       }
     }
     team_sync<TW>(team);
@@ -761,6 +770,290 @@ __global__ void __launch_bounds__(walk_cta_threads<TW>(), TW == 1 ? kWalkMinBloc
     atomicAdd(A.stat + 1, *walked);
     atomicAdd(A.stat + 2, *enumerated);
     if (twarp == 0) atomicAdd(A.stat, pairs);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Speculative single-chain kernel (one chain per 1024-thread CTA).
+//
+// The proposal positions and the acceptance draws are state-independent
+// streams (split(2), split(3)); only the base order depends on earlier
+// acceptances, and most proposals are rejected. Each round therefore
+// evaluates the next D proposals all against the CURRENT order (their rows
+// in parallel, one warp per rescanned row), then commits them in sequence
+// exactly as run_mcmc would (sampler.cpp:92-111): total, mh_accept, tracker
+// offer, trace row — up to and including the first accepted proposal, whose
+// graph becomes the state. Later proposals of the round were evaluated on a
+// stale order and are discarded; both streams are rewound to just after the
+// last committed iteration. Results are the reference's bit for bit.
+#ifndef BNMC_SPEC_D
+#define BNMC_SPEC_D 4
+#endif
+constexpr int kSpecD = BNMC_SPEC_D;  // proposals evaluated per round
+
+struct SpecSlot {
+  uint8_t prop[64], ppos[64];
+  uint8_t pv[64], pp[64], pt[64], pd[64];
+  uint64_t pc[64];
+  uint64_t pm[64];
+  double pb[64];
+  uint64_t rng_after, arng_after;
+  double thr, total;
+  int a, b, np, first;  // first: index of this slot's first pair in the flat list
+  uint8_t acc, amb;
+};
+
+__global__ void __launch_bounds__(1024, 1) walk_spec_kernel(WalkArgs A) {
+  constexpr int kThreads = 1024, kWarps = kThreads / 32;
+  __shared__ uint64_t s_bt[65 * 9];
+  __shared__ uint64_t s_boff[9];
+  __shared__ unsigned long long s_stat[kWarps][2];
+  __shared__ SpecSlot s_sl[kSpecD];
+  __shared__ uint8_t s_order[64];
+  __shared__ uint64_t s_cm[64];
+  __shared__ double s_cb[64];
+  __shared__ uint64_t s_tied, s_rng, s_arng;
+  __shared__ double s_cur_total;
+  __shared__ unsigned long long s_acc;
+  __shared__ int s_tcount, s_amb, s_d, s_npairs, s_done_to;
+  __shared__ double s_tcache[2];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int c = blockIdx.x;
+  const int n = A.n;
+  for (int i = tid; i < 65 * 9; i += kThreads) s_bt[i] = binom(i / 9, i % 9);
+  if (tid < 9) {
+    uint64_t o = 0;
+    for (int j = tid + 1; j <= A.s; ++j) o += binom(A.n - 1, j);
+    s_boff[tid] = o;
+  }
+  if (tid < 2 * kWarps) (&s_stat[0][0])[tid] = 0;
+  if (tid == 0) {
+    const Rng master{A.seeds[c]};
+    Rng init = master.split(1);  // initial order: shuffle (sampler.cpp:83-86)
+    for (int i = 0; i < n; ++i) s_order[i] = (uint8_t)i;
+    for (int i = n; i > 1; --i) {
+      const int j = (int)init.next_below((uint64_t)i);
+      const uint8_t t = s_order[i - 1];
+      s_order[i - 1] = s_order[j];
+      s_order[j] = t;
+    }
+    s_rng = master.split(2).s;
+    s_arng = master.split(3).s;
+    for (int i = 0; i < 64; ++i) {
+      s_cm[i] = 0;
+      s_cb[i] = 0.0;
+    }
+    s_tied = 0;
+    s_tcount = 0;
+    s_tcache[0] = -INFINITY;
+    s_tcache[1] = -INFINITY;
+    s_acc = 0;
+    s_amb = 0;
+    s_cur_total = 0.0;
+  }
+  __syncthreads();
+  unsigned long long* walked = &s_stat[warp][0];
+  unsigned long long* enumerated = &s_stat[warp][1];
+  unsigned long long pairs = 0;
+  uint64_t t = 0;  // iterations committed so far (0 = initial order not yet scored)
+  while (t <= A.iters) {
+    // ---- proposals of this round (thread 0): positions and accept draws
+    if (tid == 0) {
+      const int d = t == 0 ? 1 : (int)min((uint64_t)kSpecD, A.iters - t + 1);
+      Rng pr{s_rng}, ar{s_arng};
+      for (int i = 0; i < d; ++i) {
+        SpecSlot& S = s_sl[i];
+        if (t == 0) {
+          S.a = 0;
+          S.b = n - 1;
+          S.thr = 0.0;
+        } else {
+          int a = (int)pr.next_below((uint64_t)n);  // propose_swap, sampler.cpp:43-52
+          int b = (int)pr.next_below((uint64_t)(n - 1));
+          if (b >= a) ++b;
+          S.a = a;
+          S.b = b;
+          const uint64_t it = t + i;
+          if (A.thr) {
+            S.thr = A.thr[(uint64_t)c * (A.iters + 1) + it];
+            ar.next_u64();  // keep the device stream in step (unused with host thresholds)
+          } else {
+            S.thr = log10(ar.next_unit_open());
+          }
+        }
+        S.rng_after = pr.s;
+        S.arng_after = ar.s;
+        S.amb = 0;
+      }
+      s_d = d;
+    }
+    __syncthreads();
+    const int d = s_d;
+    // ---- proposed orders (every slot swaps two positions of the CURRENT order)
+    for (int idx = tid; idx < d * 64; idx += kThreads) {
+      const int i = idx >> 6, p = idx & 63;
+      if (p >= n) continue;
+      SpecSlot& S = s_sl[i];
+      const int src = t == 0 ? p : (p == S.a ? S.b : (p == S.b ? S.a : p));
+      S.prop[p] = s_order[src];
+      S.pm[p] = s_cm[p];
+      S.pb[p] = s_cb[p];
+    }
+    __syncthreads();
+    // ---- pair lists, one warp per slot (positions lo..hi + exact-tie rows)
+    if (warp < d) {
+      SpecSlot& S = s_sl[warp];
+      const int lo = t > 0 ? min(S.a, S.b) : 0, hi = t > 0 ? max(S.a, S.b) : n - 1;
+      uint64_t bit[2];
+      bool take[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int p = 2 * lane + h;
+        bit[h] = p < n ? 1ull << S.prop[p] : 0ull;
+        take[h] = p < n && ((p >= lo && p <= hi) || (p > hi && (s_tied & bit[h])));
+      }
+      uint64_t incl = bit[0] | bit[1];
+      int cnt = (int)take[0] + (int)take[1];
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const uint64_t o = __shfl_up_sync(0xffffffffu, incl, off);
+        const int kk = __shfl_up_sync(0xffffffffu, cnt, off);
+        if (lane >= off) {
+          incl |= o;
+          cnt += kk;
+        }
+      }
+      int slot = cnt - (int)take[0] - (int)take[1];
+      const uint64_t pre0 = incl & ~(bit[0] | bit[1]);
+      const uint64_t pre[2] = {pre0, pre0 | bit[0]};
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int p = 2 * lane + h;
+        if (p >= n) continue;
+        const int v = S.prop[p];
+        S.ppos[v] = (uint8_t)p;
+        if (!take[h]) continue;
+        S.pv[slot] = (uint8_t)v;
+        S.pp[slot] = (uint8_t)p;
+        S.pc[slot] = nodes_to_cand(pre[h], v);
+        S.pd[slot] = (uint8_t)(t > 0 && p > lo && p < hi && (p <= A.pe || A.yeff) &&
+                               !((s_tied >> v) & 1ull) && !((s_cm[v] >> S.prop[hi]) & 1ull));
+        ++slot;
+      }
+      if (lane == 31) S.np = cnt;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      int f = 0;
+      for (int i = 0; i < d; ++i) {
+        s_sl[i].first = f;
+        f += s_sl[i].np;
+      }
+      s_npairs = f;
+    }
+    __syncthreads();
+    // ---- every rescanned row of every slot, one warp per pair
+    const int total_pairs = s_npairs;
+    for (int q = warp; q < total_pairs; q += kWarps) {
+      int i = 0;
+      while (i + 1 < d && q >= s_sl[i + 1].first) ++i;
+      SpecSlot& S = s_sl[i];
+      const int qi = q - S.first;
+      const int v = S.pv[qi];
+      const int lo = t > 0 ? min(S.a, S.b) : 0;
+      DeltaIn dl;
+      dl.on = S.pd[qi] != 0;
+      dl.ypos = lo;
+      dl.ynode = S.prop[lo];
+      dl.old_eff = s_cb[v];
+      dl.old_cm = nodes_to_cand(s_cm[v], v);
+      const PairOut o = pair_argmax<4, 8>(A, v, S.pp[qi], S.pc[qi], S.prop, S.ppos, s_bt, s_boff, dl,
+                                          walked, enumerated);
+      if (lane == 0) {
+        S.pm[v] = cand_to_nodes(o.cm, v);
+        S.pb[v] = o.eff;
+        S.pt[qi] = (uint8_t)o.tied;
+      }
+    }
+    __syncthreads();
+    // ---- totals and mh_accept of every slot in parallel (warp i, slot i): until
+    // the first acceptance every slot compares against the same current total
+    if (warp < d && lane == 0) {
+      SpecSlot& S = s_sl[warp];
+      const uint64_t it = t + warp;
+      double tot = 0.0;  // ascending node order, engine.cpp:95-96
+      for (int j = 0; j < n; ++j) tot += S.pb[j];
+      S.total = tot;
+      const double delta = tot - s_cur_total;
+      S.acc = (uint8_t)(it == 0 || S.thr < delta);  // mh_accept, sampler.cpp:54-56
+      if (it > 0 && !A.thr) {
+        const double tol = fabs(S.thr) * A.accept_tol;
+        if (!(S.thr + tol < delta) && !(S.thr - tol >= delta)) S.amb = 1;
+      }
+    }
+    __syncthreads();
+    // ---- commit in sequence (warp 0) up to and including the first acceptance
+    if (warp == 0) {
+      int committed = d;
+      for (int i = 0; i < d; ++i)
+        if (s_sl[i].acc) {
+          committed = i + 1;
+          break;
+        }
+      for (int i = 0; i < committed; ++i) {
+        SpecSlot& S = s_sl[i];
+        const uint64_t it = t + i;
+        const bool acc = S.acc != 0;
+        if (lane == 0 && S.amb) s_amb = 1;
+        if (it == 0 || acc || !A.strict)
+          tracker_offer_warp(A.tmasks + (uint64_t)c * A.K * n, A.ttotals + (uint64_t)c * A.K,
+                             A.thash + (uint64_t)c * A.K, A.K, n, S.pm, S.total, &s_tcount, s_tcache);
+        if (lane == 0 && it > 0) {
+          const uint64_t o = (uint64_t)c * A.iters + (it - 1);
+          A.tr_prop[o] = S.total;
+          A.tr_acc[o] = acc ? 1 : 0;
+          A.tr_best[o] = s_tcache[0];
+        }
+        pairs += (unsigned long long)S.np;
+      }
+      SpecSlot& L = s_sl[committed - 1];
+      if (L.acc) {
+        for (int j = lane; j < n; j += 32) {
+          s_cm[j] = L.pm[j];
+          s_cb[j] = L.pb[j];
+          s_order[j] = L.prop[j];
+        }
+        if (lane == 0) {
+          uint64_t tn = s_tied;
+          for (int q = 0; q < L.np; ++q) {
+            const uint64_t bb = 1ull << L.pv[q];
+            tn = L.pt[q] ? (tn | bb) : (tn & ~bb);
+          }
+          s_tied = tn;
+          s_cur_total = L.total;
+          if (t + committed - 1 > 0) ++s_acc;
+        }
+      }
+      if (lane == 0) {
+        s_rng = L.rng_after;
+        s_arng = L.arng_after;
+        s_done_to = committed;
+      }
+    }
+    __syncthreads();
+    t += s_done_to;
+  }
+  if (tid < n) A.final_order[(uint64_t)c * n + tid] = s_order[tid];
+  if (tid == 0) {
+    A.final_score[c] = s_cur_total;
+    A.accepted[c] = s_acc;
+    A.tcount[c] = s_tcount;
+    if (A.ambiguous) A.ambiguous[c] = s_amb;
+    if (A.stat) atomicAdd(A.stat, pairs);
+  }
+  if (lane == 0 && A.stat) {
+    atomicAdd(A.stat + 1, *walked);
+    atomicAdd(A.stat + 2, *enumerated);
   }
 }
 
