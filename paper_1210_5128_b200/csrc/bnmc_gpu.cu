@@ -643,7 +643,8 @@ void launch_walk(bnmc_table* t, const WalkArgs& A, int C, int team_warps = 0) {
     const char* e = std::getenv("BNMC_NO_SPEC");
     return e && e[0] == '1';
   }();
-  if (tw == 32 && A.perms == nullptr && !no_spec) {
+  // speculation pays once chains settle (lower acceptance): long runs only
+  if (tw == 32 && A.perms == nullptr && !no_spec && A.iters >= 1000) {
     // few chains: one 1024-thread CTA per chain evaluating kSpecD proposals per round
     walk_spec_kernel<<<C, 1024, 0, t->stream>>>(A);
     CK(cudaGetLastError());

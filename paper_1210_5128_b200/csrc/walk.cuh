@@ -432,6 +432,7 @@ __device__ PairOut pair_argmax(const WalkArgs& A, int v, int p, uint64_t cpred, 
 // BestGraphTracker::update (sampler.cpp:32-41) by one warp: dedupe by full
 // graph equality, reject when full and total <= the minimum, insert at the
 // lower bound of (total desc, Dag operator< over the parent masks).
+template <bool kCache>
 __device__ __noinline__ void tracker_insert_warp(uint64_t* tm, double* tt, uint64_t* th, int K, int n,
                                                  const uint64_t* pm, double proposed, int* tcount,
                                                  double* tcache) {
@@ -489,19 +490,28 @@ __device__ __noinline__ void tracker_insert_warp(uint64_t* tm, double* tt, uint6
     th[ins] = h;
     const int cnt = full ? count : count + 1;
     *tcount = cnt;
-    tcache[0] = tt[0];                                // best (trace rows)
-    tcache[1] = cnt == K ? tt[K - 1] : -INFINITY;     // admission threshold when full
+    if constexpr (kCache) {
+      tcache[0] = tt[0];                                // best (trace rows)
+      tcache[1] = cnt == K ? tt[K - 1] : -INFINITY;     // admission threshold when full
+    }
   }
   __syncwarp();
 }
 
-// tcache (shared): [0] tracker best, [1] minimum when full (else -inf), kept
-// current by the insert so the common rejection needs no global load.
+// kCache: tcache (shared) holds [0] the tracker best and [1] its minimum when
+// full (else -inf), kept current by the insert so the common rejection needs
+// no global load (single-chain kernel); otherwise the tracker is read directly.
+template <bool kCache>
 __device__ __forceinline__ void tracker_offer_warp(uint64_t* tm, double* tt, uint64_t* th, int K, int n,
                                                    const uint64_t* pm, double proposed, int* tcount,
                                                    double* tcache) {
-  if (proposed <= tcache[1]) return;  // full: not above the minimum
-  tracker_insert_warp(tm, tt, th, K, n, pm, proposed, tcount, tcache);
+  if constexpr (kCache) {
+    if (proposed <= tcache[1]) return;  // full: not above the minimum
+  } else {
+    const int count = *tcount;
+    if (count == K && proposed <= tt[count - 1]) return;
+  }
+  tracker_insert_warp<kCache>(tm, tt, th, K, n, pm, proposed, tcount, tcache);
 }
 
 // Barrier over the TW warps of one team (a team runs one chain).
@@ -529,7 +539,6 @@ struct TeamState {
   double cb[64];                   // current per-node bests
   uint64_t tied, tied_new, rng, arng;
   double total, cur_total;
-  double tcache[2];                // tracker best, admission threshold
   unsigned long long acc;
   int np, a, b, accept, tcount, amb;
 };
@@ -587,8 +596,6 @@ __global__ void __launch_bounds__(walk_cta_threads<TW>(), TW == 1 ? kWalkMinBloc
     S.tied = 0;
     S.amb = 0;
     S.tcount = 0;
-    S.tcache[0] = -INFINITY;
-    S.tcache[1] = -INFINITY;
     S.acc = 0;
     S.cur_total = 0.0;
   }
@@ -733,8 +740,8 @@ __global__ void __launch_bounds__(walk_cta_threads<TW>(), TW == 1 ? kWalkMinBloc
     const bool accepted = S.accept;
     // ---- BestGraphTracker::update; every proposal is offered unless strict
     if (twarp == 0 && (t == 0 || accepted || !A.strict))
-      tracker_offer_warp(A.tmasks + (uint64_t)c * A.K * n, A.ttotals + (uint64_t)c * A.K,
-                         A.thash + (uint64_t)c * A.K, A.K, n, S.pm, proposed, &S.tcount, S.tcache);
+      tracker_offer_warp<false>(A.tmasks + (uint64_t)c * A.K * n, A.ttotals + (uint64_t)c * A.K,
+                                A.thash + (uint64_t)c * A.K, A.K, n, S.pm, proposed, &S.tcount, nullptr);
     // ---- commit + trace row
     if (accepted)
       for (int i = ttid; i < n; i += TW * 32) {
@@ -752,7 +759,7 @@ __global__ void __launch_bounds__(walk_cta_threads<TW>(), TW == 1 ? kWalkMinBloc
         const uint64_t o = (uint64_t)c * A.iters + (t - 1);
         A.tr_prop[o] = proposed;
         A.tr_acc[o] = accepted ? 1 : 0;
-        A.tr_best[o] = S.tcache[0];
+        A.tr_best[o] = A.ttotals[(uint64_t)c * A.K];
       }
     }
     team_sync<TW>(team);
@@ -1006,8 +1013,8 @@ __global__ void __launch_bounds__(1024, 1) walk_spec_kernel(WalkArgs A) {
         const bool acc = S.acc != 0;
         if (lane == 0 && S.amb) s_amb = 1;
         if (it == 0 || acc || !A.strict)
-          tracker_offer_warp(A.tmasks + (uint64_t)c * A.K * n, A.ttotals + (uint64_t)c * A.K,
-                             A.thash + (uint64_t)c * A.K, A.K, n, S.pm, S.total, &s_tcount, s_tcache);
+          tracker_offer_warp<true>(A.tmasks + (uint64_t)c * A.K * n, A.ttotals + (uint64_t)c * A.K,
+                                   A.thash + (uint64_t)c * A.K, A.K, n, S.pm, S.total, &s_tcount, s_tcache);
         if (lane == 0 && it > 0) {
           const uint64_t o = (uint64_t)c * A.iters + (it - 1);
           A.tr_prop[o] = S.total;
