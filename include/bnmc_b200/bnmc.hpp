@@ -432,8 +432,8 @@ McmcResult run_mcmc(const Dataset& data, const RunConfig& cfg, const PriorMatrix
                     const ScoreCache* prebuilt = nullptr);
 
 // ---- B200 extension: independent chains, chain c == run_mcmc with
-// cfg.seed = seeds[c], stepped in lockstep in one device loop (<= 64 per call;
-// longer seed lists are processed in groups of 64).
+// cfg.seed = seeds[c], all run by one device launch (seed lists above 65,536
+// are processed in groups of that size).
 std::vector<McmcResult> run_chains(const ScoreCache& cache, const PriorMatrix& priors,
                                    const RunConfig& cfg, std::span<const std::uint64_t> seeds);
 

@@ -548,7 +548,9 @@ std::vector<McmcResult> run_chains(const ScoreCache& cache, const PriorMatrix& p
   const std::uint64_t iters = cfg.iterations;
   std::vector<McmcResult> out;
   out.reserve(seeds.size());
-  constexpr std::size_t kGroup = 64;
+  // one device call for any number of chains (the sorted-walk path has no
+  // per-call chain limit); groups only bound the host staging buffers
+  constexpr std::size_t kGroup = std::size_t{1} << 16;
   for (std::size_t c0 = 0; c0 < seeds.size(); c0 += kGroup) {
     const int C = static_cast<int>(std::min(kGroup, seeds.size() - c0));
     std::vector<double> tp(C * iters), tb(C * iters), fs(C), tt(static_cast<std::size_t>(C) * K);
