@@ -346,3 +346,45 @@ def test_randomized_instances_all_paths():
                     o = port.run_mcmc(t, s, 60, seed, pri)
                     np.testing.assert_array_equal(rs[c].trace_proposed, o["trace_proposed"])
                     np.testing.assert_array_equal(rs[c].tracker_masks, o["tracker_masks"])
+
+
+@pytest.mark.parametrize("strict", [False, True])
+@pytest.mark.parametrize("tol,exact", [(0, 0), (30, 0), (0, 1)])
+def test_speculative_single_chain_kernel(strict, tol, exact):
+    """Few chains and >= 1000 iterations run the speculative kernel (4
+    proposals per round against the current order, committed in run_mcmc
+    order). Strict and default trackers, device acceptance (with every chain
+    forced through the exact replay) and host thresholds: all equal the
+    oracle; plus a tie-heavy instance."""
+    import ctypes as C
+    data, pri, cfg, _ = P.baseline_instance("cfg2")
+    rng = np.random.default_rng(3)
+    pri = np.where(rng.random((20, 20)) < 0.2, rng.choice([0.1, 0.9], (20, 20)), 0.5)
+    cache = P.ScoreCache.build(data, cfg, pri)
+    cfg.iterations, cfg.scan_mode, cfg.strict_paper_tracker = 1200, 2, strict
+    cfg.exact_accept, cfg.accept_tol_log2 = exact, tol
+    seeds = [5, 6]
+    rs = P.run_chains(cache, pri, seeds, cfg)
+    rep = C.c_uint64()
+    _lib.check(_lib.lib().bnmc_gpu_last_replayed(cache.handle, C.byref(rep)))
+    if tol == 30:
+        assert rep.value == len(seeds)
+    t = cache.table()
+    for c, seed in enumerate(seeds):
+        o = port.run_mcmc(t, 4, 1200, seed, pri, strict=strict)
+        np.testing.assert_array_equal(rs[c].trace_proposed, o["trace_proposed"])
+        np.testing.assert_array_equal(rs[c].trace_accepted, o["trace_accepted"])
+        np.testing.assert_array_equal(rs[c].trace_best, o["trace_best"])
+        np.testing.assert_array_equal(rs[c].tracker_masks, o["tracker_masks"])
+        np.testing.assert_array_equal(rs[c].final_order, o["final_order"])
+        assert rs[c].accepted == o["accepted"] and rs[c].final_score == o["final_score"]
+    if tol == 0 and exact == 0 and not strict:
+        cells, cards = rand_instance(21, 14, 3, cmax=2)
+        c2 = P.RunConfig(max_parents=3, gamma=1.0, iterations=1100, scan_mode=2)
+        cc = P.ScoreCache.build(P.Dataset(cards, cells), c2)
+        r2 = P.run_chains(cc, None, [1, 2], c2)
+        t2 = port.cache_build(cells, cards, 3, 1.0, 1.0)
+        for c, seed in enumerate([1, 2]):
+            o = port.run_mcmc(t2, 3, 1100, seed)
+            np.testing.assert_array_equal(r2[c].trace_proposed, o["trace_proposed"])
+            np.testing.assert_array_equal(r2[c].tracker_masks, o["tracker_masks"])
