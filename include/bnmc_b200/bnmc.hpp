@@ -263,6 +263,13 @@ class CountTable {
 
 CountTable count_statistics(const Dataset& data, int node, ParentSet pset);
 
+// Log10 BD local score of given counts (scoring.cpp:111-135) — host formula
+// over glibc lgamma in the reference's summation order (bit-identical); the
+// table build itself runs on the device (ScoreCache::build).
+double local_score_from_counts(const CountTable& counts, int pset_size, const Hyperparams& hyper);
+// count_statistics on the device + local_score_from_counts.
+double local_score(int node, ParentSet pset, const Dataset& data, const Hyperparams& hyper);
+
 double ppf(double r_value);
 
 class PpfTable {

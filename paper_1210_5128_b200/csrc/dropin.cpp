@@ -270,6 +270,32 @@ CountTable count_statistics(const Dataset& data, int node, ParentSet pset) {
   return t;
 }
 
+double local_score_from_counts(const CountTable& counts, int pset_size, const Hyperparams& hyper) {
+  // scoring.cpp:111-135: configs ascending with N_ik > 0, states ascending with
+  // c > 0, score starts at |pi| * log10(gamma) (int x double).
+  const double a_cell = hyper.alpha_cell(counts.configs(), counts.child_card());
+  if (!(a_cell > 0.0)) throw UsageError("Dirichlet hyperparameter must be positive");
+  const double a_row = a_cell * counts.child_card();
+  const double lg_row = log10_gamma(a_row), lg_cell = log10_gamma(a_cell);
+  const int card = counts.child_card();
+  double score = pset_size * std::log10(hyper.gamma);
+  counts.for_each_active([&](std::uint64_t, const std::uint32_t* row) {
+    std::uint32_t n_ik = 0;
+    double inner = 0.0;
+    for (int j = 0; j < card; ++j)
+      if (row[j] > 0) {
+        inner += log10_gamma(row[j] + a_cell) - lg_cell;
+        n_ik += row[j];
+      }
+    score += lg_row - log10_gamma(a_row + n_ik) + inner;
+  });
+  return score;
+}
+
+double local_score(int node, ParentSet pset, const Dataset& data, const Hyperparams& hyper) {
+  return local_score_from_counts(count_statistics(data, node, pset), pset.size(), hyper);
+}
+
 double ppf(double r_value) {  // scoring.cpp:143-148
   const double d = r_value - 0.5;
   return 100.0 * d * d * d;

@@ -249,6 +249,22 @@ TEST_CASE("count_statistics is bit-exact with the oracle", true) {
   }
 }
 
+TEST_CASE("local_score: device counts + reference formula, bit-exact", true) {  // test_scoring.cpp:69-118
+  const Dataset d = synth(9, 300, 12, 3);
+  const Hyperparams bdeu{0.1, 1.0, AlphaMode::kBdeu}, k2{0.5, 2.0, AlphaMode::kK2};
+  for (const Hyperparams& h : {bdeu, k2})
+    for (std::uint64_t mask : {0ull, 0x4ull, 0x1A2ull, 0x14Cull}) {
+      const ParentSet ps{mask & ~2ull};
+      double ref = 0.0;
+      REQUIRE(orc_local_score(d.cells().data(), d.cardinalities().data(), d.n(), d.rows(), 1,
+                              ps.mask, h.gamma, h.ess, h.alpha_mode == AlphaMode::kK2, &ref) == 0);
+      CHECK(same_bits(local_score(1, ps, d, h), ref));
+    }
+  // m = 0: |pi| * log10(gamma) (test_scoring.cpp:74-78)
+  const Dataset empty({2, 2, 2}, {});
+  CHECK(local_score(0, ParentSet::of({1, 2}), empty, bdeu) == 2 * std::log10(0.1));
+}
+
 TEST_CASE("capacity and usage errors", true) {
   const Dataset d = synth(9, 50, 1);
   RunConfig cfg;
