@@ -178,6 +178,12 @@ struct RunConfig {
   void validate() const;
 };
 
+// DAG utilities (types.cpp:123-164): acyclicity, order consistency, Kahn's
+// topological order with the lowest-index tie-break (DataError on a cycle).
+bool is_acyclic(const Dag& dag);
+bool consistent(ParentSet pset, int node, const Order& order);
+Order topological_order(const Dag& dag);
+
 // -------------------------------------------------------------- rng.hpp
 // splitmix64 streams (rng.hpp:14-45): the proposal and acceptance streams the
 // device loop consumes are derived exactly like this.
@@ -222,6 +228,41 @@ inline ParentSet apply_candidates(std::uint64_t position_mask, std::span<const i
   ParentSet out;
   for (std::uint64_t m = position_mask; m; m &= m - 1) out.add(candidates[std::countr_zero(m)]);
   return out;
+}
+
+// 1-based k-combinations of {1..n} (combinatorics.hpp:38-57): unrank by the
+// lexicographic rank l in [1, C(n,k)] (std::out_of_range otherwise) and back.
+struct Combination {
+  std::vector<int> elems;
+  int k() const { return static_cast<int>(elems.size()); }
+  friend bool operator==(const Combination& a, const Combination& b) { return a.elems == b.elems; }
+};
+Combination unrank_combination(int n, int k, std::uint64_t l);
+std::uint64_t rank_combination(const Combination& c, int n);
+
+// Every subset of {0..candidates-1} with size <= s, in global_index order
+// (combinatorics.hpp:81-111), as position masks / through a candidate list.
+template <class F>
+void enumerate_bounded_position_sets(int candidates, int s, F&& f) {
+  const std::uint64_t total = bounded_subset_count(candidates, s);
+  for (std::uint64_t g = 0; g < total; ++g) f(subset_at(g, candidates, s));
+}
+template <class F>
+void enumerate_bounded_subsets(std::span<const int> candidates, int s, F&& f) {
+  enumerate_bounded_position_sets(static_cast<int>(candidates.size()), s,
+                                  [&](ParentSet pos) { f(apply_candidates(pos.mask, candidates)); });
+}
+
+// Parent set table (combinatorics.hpp:113-131): row i = subset_at(i).
+struct ParentSetTable {
+  int candidates = 0;
+  int s = 0;
+  std::vector<std::uint64_t> masks;
+  std::uint64_t size() const { return masks.size(); }
+};
+ParentSetTable build_pst(int candidates, int s);
+inline std::uint64_t pst_bytes_upper_bound(int candidates, int s) {
+  return bounded_subset_count(candidates, s) * 16;
 }
 
 // ---------------------------------------------------------- scoring.hpp

@@ -192,6 +192,45 @@ void RunConfig::validate() const {  // types.cpp:111-121
   if (tasks_per_node < 0) throw UsageError("tasks-per-node must be >= 0");
 }
 
+bool is_acyclic(const Dag& dag) {
+  try {
+    topological_order(dag);
+    return true;
+  } catch (const DataError&) {
+    return false;
+  }
+}
+
+bool consistent(ParentSet pset, int node, const Order& order) {
+  const std::vector<int> pos = order.positions();
+  bool ok = true;
+  pset.for_each([&](int p) { ok = ok && pos[p] < pos[node]; });
+  return ok;
+}
+
+Order topological_order(const Dag& dag) {
+  // Kahn's procedure; the ready set is scanned for its lowest node, which is
+  // the min-heap tie-break of types.cpp:140-163.
+  const int n = dag.n();
+  std::vector<int> indeg(n);
+  for (int i = 0; i < n; ++i) indeg[i] = dag.parents(i).size();
+  std::uint64_t ready = 0, done = 0;
+  for (int i = 0; i < n; ++i)
+    if (indeg[i] == 0) ready |= std::uint64_t{1} << i;
+  std::vector<int> perm;
+  perm.reserve(n);
+  while (ready) {
+    const int v = std::countr_zero(ready);
+    ready &= ready - 1;
+    done |= std::uint64_t{1} << v;
+    perm.push_back(v);
+    for (int child = 0; child < n; ++child)
+      if (dag.parents(child).contains(v) && --indeg[child] == 0) ready |= std::uint64_t{1} << child;
+  }
+  if (static_cast<int>(perm.size()) != n) throw DataError("graph contains a cycle");
+  return Order(std::move(perm));
+}
+
 // ======================================================== combinatorics
 std::uint64_t binomial(int n, int k) {
   if (n < 0 || n > kMaxNodes || k < 0 || k > n) return 0;
@@ -237,6 +276,41 @@ ParentSet subset_at(std::uint64_t index, int candidates, int s) {
     p.add(x);
   }
   return p;
+}
+
+Combination unrank_combination(int n, int k, std::uint64_t l) {  // combinatorics.cpp:8-39
+  if (n < 0 || k < 0 || k > n) throw std::out_of_range("unrank_combination: need 0 <= k <= n");
+  if (l < 1 || l > binomial(n, k))
+    throw std::out_of_range("unrank_combination: rank " + std::to_string(l) + " outside [1, C(" +
+                            std::to_string(n) + "," + std::to_string(k) + ")]");
+  // with s = k the size-k class comes first in the global order, so the
+  // 0-based lexicographic rank is the global index; elements reported 1-based
+  const ParentSet p = subset_at(l - 1, n, k);
+  Combination c;
+  p.for_each([&](int x) { c.elems.push_back(x + 1); });
+  return c;
+}
+
+std::uint64_t rank_combination(const Combination& c, int n) {  // combinatorics.cpp:41-59
+  int prev = 0;
+  ParentSet p;
+  for (const int e : c.elems) {
+    if (e <= prev || e > n) throw std::out_of_range("rank_combination: combination invalid over n");
+    prev = e;
+    p.add(e - 1);
+  }
+  // global_index over size c.k() only: no larger size classes before it
+  return global_index(p, n, c.k()) + 1;
+}
+
+ParentSetTable build_pst(int candidates, int s) {  // combinatorics.cpp:92-101
+  ParentSetTable t;
+  t.candidates = candidates;
+  t.s = s;
+  const std::uint64_t total = bounded_subset_count(candidates, s);
+  t.masks.reserve(total);
+  for (std::uint64_t g = 0; g < total; ++g) t.masks.push_back(subset_at(g, candidates, s).mask);
+  return t;
 }
 
 // ============================================================= scoring

@@ -107,6 +107,51 @@ TEST_CASE("global_index / subset_at agree with the oracle", false) {
   CHECK(subset_at(bounded_subset_count(6, 3) - 1, 6, 3).empty());
 }
 
+TEST_CASE("combinatorics: combinations, PST, bounded enumeration", false) {  // test_combinatorics.cpp
+  // worked values (n = 6, s = 4): {0,1,2,3} -> 0, empty set -> 56
+  CHECK(global_index(ParentSet::of({0, 1, 2, 3}), 6, 4) == 0);
+  CHECK(global_index(ParentSet{}, 6, 4) == 56);
+  CHECK(bounded_subset_count(6, 4) == 57);
+  for (int n : {1, 5, 9})
+    for (int k = 0; k <= n && k <= 4; ++k)
+      for (std::uint64_t l = 1; l <= binomial(n, k); ++l) {
+        const Combination c = unrank_combination(n, k, l);
+        CHECK(c.k() == k);
+        CHECK(rank_combination(c, n) == l);
+      }
+  CHECK_THROWS_AS(unrank_combination(5, 2, 0), std::out_of_range);
+  CHECK_THROWS_AS(unrank_combination(5, 2, 11), std::out_of_range);
+  CHECK_THROWS_AS(rank_combination(Combination{{2, 2}}, 5), std::out_of_range);
+  const ParentSetTable t = build_pst(12, 3);
+  CHECK(t.size() == bounded_subset_count(12, 3));
+  std::vector<std::uint64_t> ref(t.size());
+  orc_build_pst(12, 3, ref.data());
+  CHECK(t.masks == ref);
+  std::uint64_t g = 0;
+  const std::vector<int> cands{2, 5, 7, 11};
+  bool ok = true;
+  enumerate_bounded_subsets(cands, 2, [&](ParentSet p) {
+    ok &= p == apply_candidates(subset_at(g++, 4, 2).mask, cands);
+  });
+  CHECK(ok);
+  CHECK(g == bounded_subset_count(4, 2));
+  CHECK(pst_bytes_upper_bound(59, 4) == 489406ull * 16);
+}
+
+TEST_CASE("DAG utilities", false) {  // test_types.cpp
+  Dag d(4);
+  d.add_edge(2, 0);
+  d.add_edge(3, 2);
+  d.add_edge(1, 0);
+  CHECK(is_acyclic(d));
+  CHECK(topological_order(d) == Order({1, 3, 2, 0}));
+  CHECK(consistent(ParentSet::of({1, 2}), 0, Order({1, 3, 2, 0})));
+  CHECK_FALSE(consistent(ParentSet::of({3}), 2, Order({2, 3, 1, 0})));
+  d.add_edge(0, 3);
+  CHECK_FALSE(is_acyclic(d));
+  CHECK_THROWS_AS(topological_order(d), DataError);
+}
+
 TEST_CASE("propose_swap and mh_accept consume the reference streams", false) {
   Rng a(7), b(7);
   const Order o({3, 1, 0, 2, 4});
