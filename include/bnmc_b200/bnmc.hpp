@@ -24,7 +24,11 @@
 //     throws bnmc::Error on drift (the reference checks every 100 iterations;
 //     the device loop is not interrupted).
 //   * Extensions: RunConfig::device (CUDA ordinal), ScoreCache::upload /
-//     device_table(), run_chains (independent chains in one device loop).
+//     device_table(), OrderScorer::score_many, run_chains (independent chains
+//     in one device launch).
+//   * Not provided (off the hot path): the generator and evaluation
+//     of evalgen.hpp other than confusion / prior_perturbation_protocol (io.hpp),
+//     Rng::next_normal / next_gamma, full_bitvector_scan, write_cpts, count_dags.
 #ifndef BNMC_B200_BNMC_HPP
 #define BNMC_B200_BNMC_HPP
 
