@@ -209,39 +209,35 @@ __global__ void __launch_bounds__(kScan2Threads, kScan2Per > 8 ? 2 : 4) scan2_ke
   for (int i = 0; i < myrows; ++i) {
     float k[kScan2Per];
 #pragma unroll
-    for (int e = 0; e < kScan2Per; ++e) k[e] = kn[e];
-    const bool have = hn;
+    for (int e = 0; e < kScan2Per; ++e) k[e] = hn ? kn[e] : -INFINITY;  // unloaded: nothing admissible
     hn = fetch(i + 1, kn);
     const int v = s_rows[ry + i * RG];
     const int cnt = s_cnt[v];
     for (int q = 0; q < cnt; ++q) {
       const uint64_t ncp = ~a.buckets[(b * n + v) * kMaxChains + q].cpred;
-      float mx = -INFINITY;
-      int ge = -1;
-      bool tie = false;
-      if (have) {
+      // branch-free lane max: inadmissible entries become -inf (keys are finite)
+      float kk[kScan2Per];
 #pragma unroll
-        for (int e = 0; e < kScan2Per; ++e) {
-          if ((m[e] & ncp) == 0) {
-            if (k[e] > mx) {
-              mx = k[e];
-              ge = e;
-              tie = false;
-            } else if (k[e] == mx) {
-              tie = true;
-            }
-          }
-        }
-      }
-      const uint32_t ko = ge >= 0 ? ordkey(mx) : 0u;
+      for (int e = 0; e < kScan2Per; ++e) kk[e] = (m[e] & ncp) == 0 ? k[e] : -INFINITY;
+      float mx = kk[0];
+#pragma unroll
+      for (int e = 1; e < kScan2Per; ++e) mx = fmaxf(mx, kk[e]);
+      const uint32_t ko = mx != -INFINITY ? ordkey(mx) : 0u;
       const uint32_t mxw = __reduce_max_sync(0xffffffffu, ko);
       if (mxw != 0u) {
+        // only the lanes holding the warp maximum locate it: first and last
+        // entry with that key (they differ iff the lane itself holds a tie)
         const bool win = ko == mxw;
-        const uint32_t g = (uint32_t)(g0 + (ge < 0 ? 0 : ge));
-        const uint32_t ghi = __reduce_max_sync(0xffffffffu, win ? g : 0u);
-        // a lane-level tie forces glo != ghi so the step kernel resolves it
-        const uint32_t mn = win ? (tie ? (g == 0 ? 1u : g - 1u) : g) : 0xFFFFFFFFu;
-        const uint32_t glo = __reduce_min_sync(0xffffffffu, mn);
+        uint32_t glast = 0u, gfirst = 0xFFFFFFFFu;
+        if (win) {
+          uint32_t bits = 0;
+#pragma unroll
+          for (int e = 0; e < kScan2Per; ++e) bits |= (kk[e] == mx ? 1u : 0u) << e;
+          gfirst = (uint32_t)g0 + (__ffs(bits) - 1);
+          glast = (uint32_t)g0 + (31 - __clz(bits));
+        }
+        const uint32_t ghi = __reduce_max_sync(0xffffffffu, glast);
+        const uint32_t glo = __reduce_min_sync(0xffffffffu, gfirst);
         if (lane == 0) {
           atomicMax(&s_cell[i][q][0], ((unsigned long long)mxw << 32) | ghi);
           atomicMax(&s_cell[i][q][1], ((unsigned long long)mxw << 32) | (uint32_t)~glo);
