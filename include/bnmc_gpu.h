@@ -192,6 +192,13 @@ int bnmc_gpu_table_set_scan_mode(bnmc_table* t, int mode);
  * selects the per-(row, node) lists used by delta walks. */
 int bnmc_gpu_table_set_walk_params(bnmc_table* t, int64_t enum_max, int ylists);
 
+/* Capped walks (results are identical for every setting): rows with
+ * enum_max < S(p,s) <= walk_cap walk at most budget * S(p,s) sorted entries
+ * and then enumerate PST(p) (bounds the deep walks of rows with few
+ * predecessors). walk_cap < 0: default S(n-1,s) / 512; budget < 0: default
+ * 16; budget 0 disables the cap. */
+int bnmc_gpu_table_set_walk_cap(bnmc_table* t, int64_t walk_cap, int64_t budget);
+
 /* Statistics of the last sorted-walk run_chains call: (chain, row) pairs
  * rescanned, sorted entries walked, PST entries enumerated (small predecessor
  * counts), and the device time of the last per-row sort build (ms). */

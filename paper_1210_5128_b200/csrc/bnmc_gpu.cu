@@ -143,6 +143,11 @@ struct DevBuf {
 
 }  // namespace
 
+static uint64_t env_u64(const char* name, uint64_t dflt) {
+  const char* e = std::getenv(name);
+  return e && *e ? std::strtoull(e, nullptr, 10) : dflt;
+}
+
 struct bnmc_table {
   int dev = 0;
   int n = 0, s = 0;
@@ -173,8 +178,11 @@ struct bnmc_table {
   DevBuf<uint64_t> pst2;
   DevBuf<uint32_t> pst2_off;
   int pe = -1;
+  int pc = -1;  // rows with S(p,s) <= walk_cap: capped walk, then enumeration
   bool pst_ready = false;
   uint64_t enum_max = kEnumMax;  // enumerate rows with S(p,s) <= enum_max, walk the others
+  uint64_t walk_cap = env_u64("BNMC_WALK_CAP", 0);  // 0: S(n-1,s) / kWalkCapDiv
+  uint32_t walk_budget = static_cast<uint32_t>(env_u64("BNMC_WALK_BUDGET", kWalkBudget));
   int scan_mode = 0;  // default for score_orders: 0 auto (walk), 1 full-row scan
   DevBuf<int> d_fo, d_tc;
   DevBuf<unsigned long long> d_acc;
@@ -545,9 +553,14 @@ void build_pst_small(bnmc_table* t) {
   int pe = -1;
   for (int p = 0; p < t->n && bounded_count(p, t->s) <= t->enum_max; ++p) pe = p;
   t->pe = pe;
+  int pc = pe;
+  const uint64_t cap = t->walk_cap ? t->walk_cap : std::max<uint64_t>(kEnumMax, t->S / kWalkCapDiv);
+  if (t->walk_budget > 0)
+    for (int p = pe + 1; p < t->n && bounded_count(p, t->s) <= cap; ++p) pc = p;
+  t->pc = pc;
   std::vector<uint64_t> m1, m2;
   std::vector<uint32_t> o1, o2;
-  build_pst_table(t->n, t->s, pe, m1, o1);
+  build_pst_table(t->n, t->s, pc, m1, o1);
   build_pst_table(t->n, t->s - 1, std::max(pe - 1, 0), m2, o2);
   t->pst.alloc(std::max<size_t>(m1.size(), 1));
   t->pst_off.alloc(o1.size());
@@ -681,6 +694,8 @@ WalkArgs walk_args(bnmc_table* t) {
   A.pst2 = t->pst2.p;
   A.pst2_off = t->pst2_off.p;
   A.pe = t->pe;
+  A.pc = t->pc;
+  A.wbud = t->walk_budget;
   A.S = t->S;
   A.n = t->n;
   A.s = t->s;
@@ -1401,6 +1416,16 @@ int bnmc_gpu_table_set_scan_mode(bnmc_table* t, int mode) {
     if (!t) raise(BNMC_USAGE, "null table");
     if (mode < 0 || mode > 2) raise(BNMC_USAGE, "scan_mode must be 0, 1 or 2");
     t->scan_mode = mode;
+  });
+}
+
+int bnmc_gpu_table_set_walk_cap(bnmc_table* t, int64_t walk_cap, int64_t budget) {
+  return guarded([&] {
+    if (!t) raise(BNMC_USAGE, "null table");
+    if (budget > 0xFFFF) raise(BNMC_USAGE, "walk budget must be <= 65535");
+    t->walk_cap = walk_cap < 0 ? 0 : static_cast<uint64_t>(walk_cap);
+    t->walk_budget = budget < 0 ? static_cast<uint32_t>(kWalkBudget) : static_cast<uint32_t>(budget);
+    t->pst_ready = false;
   });
 }
 

@@ -51,6 +51,16 @@ constexpr int kWalkMinBlocks1 = BNMC_WALK_MINB1;  // CTAs per SM targeted for on
 #endif
 constexpr int kEnumUnroll = BNMC_ENUM_UNROLL;  // independent gathers per lane per enumeration step
 constexpr uint64_t kEnumMax = 64;          // enumerate when S(p,s) <= this (walk above)
+// Rows with kEnumMax < S(p,s) <= walk cap walk at most kWalkBudget * S(p,s)
+// sorted entries, then enumerate PST(p): bounds the deep walks of rows with
+// few predecessors (their first admissible entry can sit 10^4 deep). The cap
+// defaults to S(n-1,s) / kWalkCapDiv (measured: cfg4 1024 -> p <= 12, cfg5
+// 16384 -> p <= 18); a gathered enumeration entry costs ~15 walked entries.
+#ifndef BNMC_WALK_BUDGET_DEFAULT
+#define BNMC_WALK_BUDGET_DEFAULT 16
+#endif
+constexpr uint64_t kWalkCapDiv = 512;
+constexpr uint64_t kWalkBudget = BNMC_WALK_BUDGET_DEFAULT;
 
 struct WalkArgs {
   const double* __restrict__ seff;    // [n][Sw] eff, sorted descending per row, padded
@@ -62,11 +72,13 @@ struct WalkArgs {
   uint64_t Sy, Syw;                   // entries per list, padded stride
   const double* __restrict__ ls;      // [n][S] local scores, BNSC order
   const double* __restrict__ w;       // [n][n] PPF weights
-  const uint64_t* __restrict__ pst;   // position masks of PST(p) for p <= pe, concatenated
-  const uint32_t* __restrict__ pst_off;  // [pe+2]
+  const uint64_t* __restrict__ pst;   // position masks of PST(p) for p <= pc, concatenated
+  const uint32_t* __restrict__ pst_off;  // [pc+2]
   const uint64_t* __restrict__ pst2;  // PST(p, s-1) for p < pe: sets of the other positions
   const uint32_t* __restrict__ pst2_off;  // [pe+1]
   int pe;                              // largest enumerated predecessor count
+  int pc;                              // largest count with a capped walk (>= pe)
+  uint32_t wbud;                       // walk budget, in multiples of S(p,s)
   uint64_t S;
   int n, s;
   // chains
@@ -337,95 +349,98 @@ __device__ PairOut pair_argmax(const WalkArgs& A, int v, int p, uint64_t cpred, 
                                unsigned long long* enumerated) {
   const int lane = threadIdx.x & 31;
   PairOut r;
-  if (p <= A.pe) {
-    // delta rows: the sets containing Y only (PST(p-1, s-1) with Y's position
-    // inserted); otherwise every admissible set (PST(p, s))
-    const uint64_t* pst = d.on ? A.pst2 + A.pst2_off[p - 1] : A.pst + A.pst_off[p];
-    const uint32_t cnt = d.on ? A.pst2_off[p] - A.pst2_off[p - 1] : A.pst_off[p + 1] - A.pst_off[p];
-    r = enum_pst<EU>(A, v, pst, cnt, d.on ? d.ypos : -1, order, bt, boff);
-    if (lane == 0) *enumerated += cnt;
-    if (d.on) {
-      if (!(r.eff >= d.old_eff)) {  // also covers cnt == 0 (s == 0)
-        r.eff = d.old_eff;
-        r.cm = d.old_cm;
-        r.tied = 0;
-      } else if (r.eff == d.old_eff) {
+  if (p > A.pe) {
+    const uint64_t ncp = ~cpred;
+    if (d.on && A.yeff) {
+      // ---- delta walk: only sets containing Y can beat the current best, so
+      // walk row v's list of entries containing Y down to the current best's
+      // value (SURVEY §7 "incremental middle rows")
+      const int qy = d.ynode - (d.ynode > v);
+      const uint64_t lo = ((uint64_t)v * (A.n - 1) + qy) * A.Syw;
+      const double* ye = A.yeff + lo;
+      const uint64_t* yc = A.ycm + lo;
+      WalkHit h;
+      bool done = false;
+      uint64_t base = 0;
+      if (!walk_round<1>(ye, yc, ncp, A.Sy, base, lane, h, d.old_eff, &done) && !done &&
+          !walk_round<2>(ye, yc, ncp, A.Sy, base, lane, h, d.old_eff, &done) && !done)
+        while (base < A.Sy && !done && !walk_round<WU>(ye, yc, ncp, A.Sy, base, lane, h, d.old_eff, &done)) {
+        }
+      if (lane == 0) *walked += base;
+      r.eff = d.old_eff;
+      r.cm = d.old_cm;
+      r.tied = 0;
+      if (h.start == ~0ull) return r;  // no set containing Y reaches the current best
+      int ties = 0;
+      uint64_t cm = h.kcm;
+      if (!h.next_differs) cm = collect_ties(ye, yc, ncp, A.Sy, h.start, h.kstar, h.kcm, v, ppos, &ties);
+      if (h.kstar > d.old_eff) {
+        r.eff = h.kstar;
+        r.cm = cm;
+        r.tied = ties > 0;
+      } else {  // equal to the current best: an exact tie, position rule decides
         r.tied = 1;
-        if (prefer_pos(d.old_cm, r.cm, v, ppos)) r.cm = d.old_cm;
+        if (!prefer_pos(d.old_cm, cm, v, ppos)) r.cm = cm;
       }
+      return r;
     }
-    return r;
-  }
-  const uint64_t ncp = ~cpred;
-  if (d.on && A.yeff) {
-    // ---- delta walk: only sets containing Y can beat the current best, so
-    // walk row v's list of entries containing Y down to the current best's
-    // value (SURVEY §7 "incremental middle rows")
-    const int qy = d.ynode - (d.ynode > v);
-    const uint64_t lo = ((uint64_t)v * (A.n - 1) + qy) * A.Syw;
-    const double* ye = A.yeff + lo;
-    const uint64_t* yc = A.ycm + lo;
+    // ---- walk of the sorted row; rows with a PST(p) stop after the budget
+    // and enumerate instead
+    const double* re = A.seff + (uint64_t)v * A.Sw;
+    const uint64_t* rc = A.scm + (uint64_t)v * A.Sw;
+    const uint64_t S = A.S;
+    const uint64_t lim =
+        p <= A.pc ? (uint64_t)A.wbud * (A.pst_off[p + 1] - A.pst_off[p]) : S;
     WalkHit h;
-    bool done = false;
+    // Rounds grow 32, 64, 128, then 32 * WU entries: most first admissible
+    // entries sit in the first 32, deep walks still get WU loads per lane in flight.
     uint64_t base = 0;
-    if (!walk_round<1>(ye, yc, ncp, A.Sy, base, lane, h, d.old_eff, &done) && !done &&
-        !walk_round<2>(ye, yc, ncp, A.Sy, base, lane, h, d.old_eff, &done) && !done)
-      while (base < A.Sy && !done && !walk_round<WU>(ye, yc, ncp, A.Sy, base, lane, h, d.old_eff, &done)) {
+    if (walk_round<1>(re, rc, ncp, S, base, lane, h) || walk_round<2>(re, rc, ncp, S, base, lane, h) ||
+        walk_round<4>(re, rc, ncp, S, base, lane, h)) {
+    } else {
+      while (base < lim && base < S && !walk_round<WU>(re, rc, ncp, S, base, lane, h)) {
       }
+    }
     if (lane == 0) *walked += base;
-    r.eff = d.old_eff;
-    r.cm = d.old_cm;
-    r.tied = 0;
-    if (h.start == ~0ull) return r;  // no set containing Y reaches the current best
-    int ties = 0;
-    uint64_t cm = h.kcm;
-    if (!h.next_differs) cm = collect_ties(ye, yc, ncp, A.Sy, h.start, h.kstar, h.kcm, v, ppos, &ties);
-    if (h.kstar > d.old_eff) {
+    if (h.start != ~0ull) {
       r.eff = h.kstar;
-      r.cm = cm;
+      r.cm = h.kcm;
+      r.tied = 0;
+      // Fast exit: the entry after `start` is still in registers of this round and
+      // has a different value (exact ties are rare), so no tie is possible.
+      if (h.next_differs) return r;
+      // Tie collection (rare): admissible entries after `start` with eff == kstar.
+      int ties = 0;
+      r.cm = collect_ties(re, rc, ncp, S, h.start, h.kstar, h.kcm, v, ppos, &ties);
       r.tied = ties > 0;
-    } else {  // equal to the current best: an exact tie, position rule decides
+      return r;
+    }
+    if (p > A.pc) {  // cannot happen: the empty set is admissible in every row
+      if (lane == 0) atomicExch(A.error, 4);
+      r.eff = -INFINITY;
+      r.cm = 0;
+      r.tied = 0;
+      return r;
+    }
+  }
+  // ---- PST enumeration. Delta rows (p <= pe): the sets containing Y only
+  // (PST(p-1, s-1) with Y's position inserted); otherwise every admissible set
+  // (PST(p, s)), also after a walk that ran out of budget.
+  const bool de = d.on && p <= A.pe;
+  const uint64_t* pst = de ? A.pst2 + A.pst2_off[p - 1] : A.pst + A.pst_off[p];
+  const uint32_t cnt = de ? A.pst2_off[p] - A.pst2_off[p - 1] : A.pst_off[p + 1] - A.pst_off[p];
+  r = enum_pst<EU>(A, v, pst, cnt, de ? d.ypos : -1, order, bt, boff);
+  if (lane == 0) *enumerated += cnt;
+  if (de) {
+    if (!(r.eff >= d.old_eff)) {  // also covers cnt == 0 (s == 0)
+      r.eff = d.old_eff;
+      r.cm = d.old_cm;
+      r.tied = 0;
+    } else if (r.eff == d.old_eff) {
       r.tied = 1;
-      if (!prefer_pos(d.old_cm, cm, v, ppos)) r.cm = cm;
-    }
-    return r;
-  }
-  // ---- walk of the sorted row
-  const double* re = A.seff + (uint64_t)v * A.Sw;
-  const uint64_t* rc = A.scm + (uint64_t)v * A.Sw;
-  const uint64_t S = A.S;
-  WalkHit h;
-  // Rounds grow 32, 64, 128, then 256 entries: most first admissible entries
-  // sit in the first 32, deep walks still get 8 loads per lane in flight.
-  uint64_t base = 0;
-  if (walk_round<1>(re, rc, ncp, S, base, lane, h) || walk_round<2>(re, rc, ncp, S, base, lane, h) ||
-      walk_round<4>(re, rc, ncp, S, base, lane, h)) {
-  } else {
-    while (base < S && !walk_round<WU>(re, rc, ncp, S, base, lane, h)) {
+      if (prefer_pos(d.old_cm, r.cm, v, ppos)) r.cm = d.old_cm;
     }
   }
-  const uint64_t start = h.start;
-  const bool next_differs = h.next_differs;
-  const double kstar = h.kstar;
-  const uint64_t kcm = h.kcm;
-  if (start == ~0ull) {  // cannot happen: the empty set is admissible in every row
-    if (lane == 0) atomicExch(A.error, 4);
-    r.eff = -INFINITY;
-    r.cm = 0;
-    r.tied = 0;
-    return r;
-  }
-  if (lane == 0) *walked += base;
-  r.eff = kstar;
-  r.cm = kcm;
-  r.tied = 0;
-  // Fast exit: the entry after `start` is still in registers of this round and
-  // has a different value (exact ties are rare), so no tie is possible.
-  if (next_differs) return r;
-  // Tie collection (rare): admissible entries after `start` with eff == kstar.
-  int ties = 0;
-  r.cm = collect_ties(re, rc, ncp, S, start, kstar, kcm, v, ppos, &ties);
-  r.tied = ties > 0;
   return r;
 }
 
