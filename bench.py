@@ -260,10 +260,15 @@ def run_ours(args):
             ours1 = P.run_chains(cache, pri, [1], c1)[0]
             cpu = cpu_baseline(cache, pri, cfg, ours1.trace_proposed, args.cpu_iters, 1)
         if world == 1 and not args.no_extras:
-            c1 = P.RunConfig(max_parents=cfg.max_parents, iterations=I, scan_mode=2, team_warps=0,
+            # one chain (the reference's own unit of work): latency-bound, the
+            # speculative single-chain kernel runs at >= 1000 iterations
+            I1 = 2000
+            c1 = P.RunConfig(max_parents=cfg.max_parents, iterations=I1, scan_mode=2, team_warps=0,
                              memory_cap_bytes=cfg.memory_cap_bytes, device=local)
+            P.run_chains_batch(cache, pri, [1], c1)  # warm-up
             one = P.run_chains_batch(cache, pri, [1], c1)
-            extra["single_chain_it_s"] = I / (one.device_ms / 1e3)
+            extra["single_chain_it_s"] = I1 / (one.device_ms / 1e3)
+            extra["single_chain_iterations"] = I1
             extra["full_scan_path"] = full_scan_probe(P, _lib, cache, pri, cfg)
         h2d = 8 * Cn
         d2h = (Cn * I * (8 + 1 + 8) + Cn * K * (n * 8 + 8) + Cn * (n * 4 + 8 + 8 + 4) + 4 * Cn)

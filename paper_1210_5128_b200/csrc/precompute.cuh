@@ -123,6 +123,7 @@ __global__ void __launch_bounds__(kK1Threads) k1_kernel(K1Args a, uint64_t prefi
   __shared__ int s_p[9];
   __shared__ int s_rad[10];
   __shared__ int s_k, s_rP, s_ext0;
+  __shared__ double s_term[kK1Threads];  // per-warp scoring terms
   const int tid = threadIdx.x;
   const int n = a.n, W = a.W;
   if (tid == 0) {
@@ -268,8 +269,12 @@ __global__ void __launch_bounds__(kK1Threads) k1_kernel(K1Args a, uint64_t prefi
       c[cu - 1] = NP[cfg] - sum;
     }
     __syncthreads();
-    // Score the |U| entries (v, U - v) of every U = P + {u}.
-    for (int idx = tid; idx < ne * (k + 1); idx += kK1Threads) {
+    // Score the |U| entries (v, U - v) of every U = P + {u}: one warp per
+    // entry, lanes over the configurations of pi (their terms are
+    // independent), then lane 0 folds the terms in configuration order — the
+    // reference's serial summation (scoring.cpp:111-135) bit for bit, with
+    // the gathers of 32 configurations in flight instead of one.
+    for (int idx = warp; idx < ne * (k + 1); idx += kK1Threads / 32) {
       const int e = idx / (k + 1), d = idx - e * (k + 1);
       const int u = ext0 + e0 + e;
       const int v = d < k ? s_p[d] : u;
@@ -282,7 +287,7 @@ __global__ void __launch_bounds__(kK1Threads) k1_kernel(K1Args a, uint64_t prefi
       const uint64_t r_pi = (uint64_t)rP * cu / cv;
       const int pair = find_pair(a, r_pi * 512 + cv);
       if (pair < 0) {
-        atomicExch(a.error, 2);
+        if (lane == 0) atomicExch(a.error, 2);
         continue;
       }
       const double* lgc = a.lut + (uint64_t)pair * a.lut_stride;
@@ -290,40 +295,43 @@ __global__ void __launch_bounds__(kK1Threads) k1_kernel(K1Args a, uint64_t prefi
       const double lg_cell = lgc[0], lg_row = lgr[0];
       double score = (double)k * a.log10_gamma;  // |pi| = k, int * double first
       const uint32_t* H = CNT + e * rP * cmax;    // H[cfgP * cmax + x_u]
-      if (d == k) {
-        // child = u: configs of pi = P ascending, states of u.
-        for (int cfg = 0; cfg < rP; ++cfg) {
-          const uint32_t* row = H + cfg * cmax;
-          uint32_t n_ik = 0;
-          double inner = 0.0;
-          for (int x = 0; x < cv; ++x) {
-            const uint32_t c = row[x];
+      // child = u: configs of pi = P, H[cfg * cmax + x]; child = p_d: configs
+      // of pi = (P - p_d) + {u}, k' = low + R*(mid + Q*x_u), H[(low + R*(y +
+      // cd*mid)) * cmax + x_u]
+      const int R = d < k ? s_rad[d] : 1, Q = d < k ? rP / (R * cv) : 1;
+      const int rpi = (int)r_pi;
+      double* term = s_term + warp * 32;
+      for (int c0 = 0; c0 < rpi; c0 += 32) {
+        const int kk = c0 + lane;
+        uint32_t n_ik = 0;
+        double inner = 0.0;
+        if (kk < rpi) {
+          int base, stride;
+          if (d == k) {
+            base = kk * cmax;
+            stride = 1;
+          } else {
+            const int low = kk % R, rest = kk / R;
+            const int mid = rest % Q, xu = rest / Q;
+            base = (low + R * cv * mid) * cmax + xu;
+            stride = R * cmax;
+          }
+          for (int y = 0; y < cv; ++y) {
+            const uint32_t c = H[base + y * stride];
             if (c > 0) {
               inner += lgc[c] - lg_cell;
               n_ik += c;
             }
           }
-          if (n_ik > 0) score += lg_row - lgr[n_ik] + inner;
+          if (n_ik > 0) term[lane] = lg_row - lgr[n_ik] + inner;
         }
-      } else {
-        // child = p_d: configs of pi = (P - p_d) + {u}: k' = low + R*(mid + Q*x_u).
-        const int R = s_rad[d], cd = cv;
-        const int Q = rP / (R * cd);
-        for (int xu = 0; xu < cu; ++xu)
-          for (int mid = 0; mid < Q; ++mid)
-            for (int low = 0; low < R; ++low) {
-              uint32_t n_ik = 0;
-              double inner = 0.0;
-              for (int y = 0; y < cd; ++y) {
-                const uint32_t c = H[(low + R * (y + cd * mid)) * cmax + xu];
-                if (c > 0) {
-                  inner += lgc[c] - lg_cell;
-                  n_ik += c;
-                }
-              }
-              if (n_ik > 0) score += lg_row - lgr[n_ik] + inner;
-            }
+        const unsigned has = __ballot_sync(0xffffffffu, n_ik > 0);
+        __syncwarp();
+        if (lane == 0)
+          for (unsigned b = has; b; b &= b - 1) score += term[__ffs(b) - 1];
+        __syncwarp();
       }
+      if (lane != 0) continue;
       const uint64_t g = global_index_dev(nodes_to_cand(pmask, v), n - 1, a.s);
       a.ls[(uint64_t)v * a.S + g] = score;
     }
