@@ -327,8 +327,17 @@ __global__ void __launch_bounds__(kK1Threads) k1_kernel(K1Args a, uint64_t prefi
         }
         const unsigned has = __ballot_sync(0xffffffffu, n_ik > 0);
         __syncwarp();
-        if (lane == 0)
-          for (unsigned b = has; b; b &= b - 1) score += term[__ffs(b) - 1];
+        if (lane == 0) {
+          const int cnt = min(32, rpi - c0);
+          if (has == (cnt == 32 ? 0xffffffffu : (1u << cnt) - 1u)) {
+            // every configuration of the chunk is non-empty (the common case):
+            // loads batched ahead of the serial add chain
+#pragma unroll 8
+            for (int j = 0; j < cnt; ++j) score += term[j];
+          } else {
+            for (unsigned b = has; b; b &= b - 1) score += term[__ffs(b) - 1];
+          }
+        }
         __syncwarp();
       }
       if (lane != 0) continue;
