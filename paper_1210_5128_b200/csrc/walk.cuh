@@ -62,6 +62,12 @@ constexpr uint64_t kEnumMax = 64;          // enumerate when S(p,s) <= this (wal
 constexpr uint64_t kWalkCapDiv = 512;
 constexpr uint64_t kWalkBudget = BNMC_WALK_BUDGET_DEFAULT;
 
+// i = base, base + stride for n <= 64 nodes and stride >= 32: at most two
+// steps, written out so the compiler does not unroll a generic strided loop.
+#define BNMC_FOR_NODES(i, base, stride, n) \
+  _Pragma("unroll") for (int i##_h = 0; i##_h < 2; ++i##_h) \
+    if (const int i = (base) + i##_h * (stride); i < (n))
+
 struct WalkArgs {
   const double* __restrict__ seff;    // [n][Sw] eff, sorted descending per row, padded
   const uint64_t* __restrict__ scm;   // [n][Sw] candidate masks in the same order
@@ -456,7 +462,7 @@ __device__ __noinline__ void tracker_insert_warp(uint64_t* tm, double* tt, uint6
   const bool full = count == K;
   // graph hash: dedupe compares hashes first, masks only on a hash match
   uint64_t hv = 0;
-  for (int i = lane; i < n; i += 32) hv ^= Rng::mix(pm[i] + 0x9E3779B97F4A7C15ull * (uint64_t)(i + 1));
+  BNMC_FOR_NODES(i, lane, 32, n) hv ^= Rng::mix(pm[i] + 0x9E3779B97F4A7C15ull * (uint64_t)(i + 1));
   const uint64_t h = ((uint64_t)__reduce_xor_sync(0xffffffffu, (unsigned)(hv >> 32)) << 32) |
                      __reduce_xor_sync(0xffffffffu, (unsigned)hv);
   for (int e0 = 0; e0 < count; e0 += 32) {
@@ -466,7 +472,7 @@ __device__ __noinline__ void tracker_insert_warp(uint64_t* tm, double* tt, uint6
       const int e = e0 + __ffs(cand) - 1;
       cand &= cand - 1;
       bool eq = true;
-      for (int i = lane; i < n; i += 32) eq &= tm[(uint64_t)e * n + i] == pm[i];
+      BNMC_FOR_NODES(i, lane, 32, n) eq &= tm[(uint64_t)e * n + i] == pm[i];
       if (__all_sync(0xffffffffu, eq)) return;  // already tracked
     }
   }
@@ -492,14 +498,14 @@ __device__ __noinline__ void tracker_insert_warp(uint64_t* tm, double* tt, uint6
   }
   const int last = full ? count - 1 : count;
   for (int e = last; e > ins; --e) {  // move entries [ins, last) down one slot
-    for (int i = lane; i < n; i += 32) tm[(uint64_t)e * n + i] = tm[(uint64_t)(e - 1) * n + i];
+    BNMC_FOR_NODES(i, lane, 32, n) tm[(uint64_t)e * n + i] = tm[(uint64_t)(e - 1) * n + i];
     if (lane == 0) {
       tt[e] = tt[e - 1];
       th[e] = th[e - 1];
     }
     __syncwarp();
   }
-  for (int i = lane; i < n; i += 32) tm[(uint64_t)ins * n + i] = pm[i];
+  BNMC_FOR_NODES(i, lane, 32, n) tm[(uint64_t)ins * n + i] = pm[i];
   if (lane == 0) {
     tt[ins] = proposed;
     th[ins] = h;
