@@ -24,18 +24,21 @@ __device__ __forceinline__ uint64_t binom(int n, int k) {
 __device__ __forceinline__ int cand_node(int q, int v) { return q < v ? q : q + 1; }
 
 // Candidate-position mask -> node mask for row v.
+// Bit select with a constant shift (two LOP3 + a funnel shift): identical to
+// (cm & lm) | ((cm >> v) << (v + 1)) for every v in [0, 63].
 __device__ __forceinline__ uint64_t cand_to_nodes(uint64_t cm, int v) {
-  const uint64_t low = cm & ((1ull << v) - 1ull);
-  const uint64_t high = v < 63 ? (cm >> v) << (v + 1) : 0ull;
-  return low | high;
+  const uint64_t lm = (1ull << v) - 1ull;
+  const uint64_t lm2 = (lm << 1) | 1ull;  // bits 0..v
+  return (cm & lm) | ((cm << 1) & ~lm2);
 }
 
 // Node mask -> candidate-position mask for row v (ScoreCache::index_of,
 // scoring.hpp:135-137).
+// Identical to (pm & lm) | ((pm >> (v + 1)) << v) for every v in [0, 63]
+// (bit v of pm is dropped either way), as a bit select.
 __device__ __host__ __forceinline__ uint64_t nodes_to_cand(uint64_t pm, int v) {
-  const uint64_t low = pm & ((1ull << v) - 1ull);
-  const uint64_t high = v + 1 < 64 ? (pm >> (v + 1)) << v : 0ull;
-  return low | high;
+  const uint64_t lm = (1ull << v) - 1ull;
+  return (pm & lm) | ((pm >> 1) & ~lm);
 }
 
 // PpfTable::sum (scoring.hpp:103-107): ascending parents, starting from 0.0.
