@@ -697,6 +697,11 @@ WalkArgs walk_args(bnmc_table* t) {
   A.pc = t->pc;
   A.wbud = t->walk_budget;
   A.S = t->S;
+  if (t->Sw > 0xFFFFFFFFull || t->Syw > 0xFFFFFFFFull)  // unreachable within device memory
+    raise(BNMC_CAPACITY, "sorted rows longer than 2^32 entries");
+  A.S32 = static_cast<uint32_t>(t->S);
+  A.Sw32 = static_cast<uint32_t>(t->Sw);
+  A.Syw32 = static_cast<uint32_t>(t->Syw);
   A.n = t->n;
   A.s = t->s;
   A.stat = t->stat.p;

@@ -86,6 +86,7 @@ struct WalkArgs {
   int pc;                              // largest count with a capped walk (>= pe)
   uint32_t wbud;                       // walk budget, in multiples of S(p,s)
   uint64_t S;
+  uint32_t S32, Sw32, Syw32;  // S, Sw, Syw (< 2^32, checked on the host): 32x32->64 index math
   int n, s;
   // chains
   int C;
@@ -180,7 +181,7 @@ struct WalkHit {
 
 // One walk round of U entries per lane at sorted indices [base, base + 32U);
 // advances base; true once the first admissible entry is found.
-template <int U>
+template <int U, bool kFloor = false>
 __device__ BNMC_WALK_ROUND_INLINE bool walk_round(const double* re, const uint64_t* rc, uint64_t ncp,
                                            uint64_t S, uint64_t& base, int lane, WalkHit& h,
                                            double floor = -INFINITY, bool* exhausted = nullptr) {
@@ -199,7 +200,7 @@ __device__ BNMC_WALK_ROUND_INLINE bool walk_round(const double* re, const uint64
   unsigned hb = 0;
 #pragma unroll
   for (int u = U - 1; u >= 0; --u) {
-    const unsigned bal = __ballot_sync(0xffffffffu, (c[u] & ncp) == 0 && e[u] >= floor);
+    const unsigned bal = __ballot_sync(0xffffffffu, (c[u] & ncp) == 0 && (!kFloor || e[u] >= floor));
     if (bal) {
       hu = u;
       hb = bal;
@@ -209,7 +210,7 @@ __device__ BNMC_WALK_ROUND_INLINE bool walk_round(const double* re, const uint64
   if (hu < 0) {
     // sorted descending: once the round's last entry is below the floor, no
     // later entry can qualify
-    if (exhausted && __shfl_sync(0xffffffffu, e[U - 1], 31) < floor) *exhausted = true;
+    if (kFloor && __shfl_sync(0xffffffffu, e[U - 1], 31) < floor) *exhausted = true;
     return false;
   }
   double eh = e[0], en = U > 1 ? e[1 < U ? 1 : 0] : e[0];
@@ -297,7 +298,7 @@ __device__ __forceinline__ PairOut enum_pst(const WalkArgs& A, int v, const uint
         const uint64_t pm = (pm0 & lowm) | ((pm0 & ~lowm) << 1) | insb;
         for (uint64_t m = pm; m; m &= m - 1) nm[u] |= 1ull << order[__ffsll((long long)m) - 1];
         const uint64_t g = gidx_smem(nodes_to_cand(nm[u], v), A.n - 1, boff, bt);
-        lv[u] = __ldg(A.eff + (uint64_t)v * A.S + g);
+        lv[u] = __ldg(A.eff + (uint64_t)(uint32_t)v * A.S32 + g);
       }
     }
 #pragma unroll
@@ -362,15 +363,15 @@ __device__ PairOut pair_argmax(const WalkArgs& A, int v, int p, uint64_t cpred, 
       // walk row v's list of entries containing Y down to the current best's
       // value (SURVEY §7 "incremental middle rows")
       const int qy = d.ynode - (d.ynode > v);
-      const uint64_t lo = ((uint64_t)v * (A.n - 1) + qy) * A.Syw;
+      const uint64_t lo = (uint64_t)(uint32_t)(v * (A.n - 1) + qy) * A.Syw32;
       const double* ye = A.yeff + lo;
       const uint64_t* yc = A.ycm + lo;
       WalkHit h;
       bool done = false;
       uint64_t base = 0;
-      if (!walk_round<1>(ye, yc, ncp, A.Sy, base, lane, h, d.old_eff, &done) && !done &&
-          !walk_round<2>(ye, yc, ncp, A.Sy, base, lane, h, d.old_eff, &done) && !done)
-        while (base < A.Sy && !done && !walk_round<WU>(ye, yc, ncp, A.Sy, base, lane, h, d.old_eff, &done)) {
+      if (!walk_round<1, true>(ye, yc, ncp, A.Sy, base, lane, h, d.old_eff, &done) && !done &&
+          !walk_round<2, true>(ye, yc, ncp, A.Sy, base, lane, h, d.old_eff, &done) && !done)
+        while (base < A.Sy && !done && !walk_round<WU, true>(ye, yc, ncp, A.Sy, base, lane, h, d.old_eff, &done)) {
         }
       if (lane == 0) *walked += base;
       r.eff = d.old_eff;
@@ -392,8 +393,9 @@ __device__ PairOut pair_argmax(const WalkArgs& A, int v, int p, uint64_t cpred, 
     }
     // ---- walk of the sorted row; rows with a PST(p) stop after the budget
     // and enumerate instead
-    const double* re = A.seff + (uint64_t)v * A.Sw;
-    const uint64_t* rc = A.scm + (uint64_t)v * A.Sw;
+    const uint64_t ro = (uint64_t)(uint32_t)v * A.Sw32;
+    const double* re = A.seff + ro;
+    const uint64_t* rc = A.scm + ro;
     const uint64_t S = A.S;
     const uint64_t lim =
         p <= A.pc ? (uint64_t)A.wbud * (A.pst_off[p + 1] - A.pst_off[p]) : S;
