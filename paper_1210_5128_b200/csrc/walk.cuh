@@ -183,14 +183,14 @@ struct WalkHit {
 // advances base; true once the first admissible entry is found.
 template <int U, bool kFloor = false>
 __device__ BNMC_WALK_ROUND_INLINE bool walk_round(const double* re, const uint64_t* rc, uint64_t ncp,
-                                           uint64_t S, uint64_t& base, int lane, WalkHit& h,
+                                           uint32_t S, uint32_t& base, int lane, WalkHit& h,
                                            double floor = -INFINITY, bool* exhausted = nullptr) {
   if (base >= S) return false;
   double e[U];
   uint64_t c[U];
 #pragma unroll
   for (int u = 0; u < U; ++u) {
-    const uint64_t i = base + u * 32 + lane;  // < Sw: rows are padded by one round
+    const uint32_t i = base + u * 32 + lane;  // < Sw < 2^32: rows are padded by one round
     e[u] = __ldg(re + i);
     c[u] = __ldg(rc + i);
   }
@@ -223,7 +223,7 @@ __device__ BNMC_WALK_ROUND_INLINE bool walk_round(const double* re, const uint64
       en = e[u + 1 < U ? u + 1 : u];
     }
   const int f = __ffs(hb) - 1;
-  h.start = base - 32 * U + hu * 32 + f;
+  h.start = (uint64_t)(base - 32 * U + hu * 32 + f);
   h.kstar = shfl_d(eh, f);
   h.kcm = shfl_u64(ch, f);
   // value of the next sorted entry, when it is in this round's registers
@@ -368,10 +368,11 @@ __device__ PairOut pair_argmax(const WalkArgs& A, int v, int p, uint64_t cpred, 
       const uint64_t* yc = A.ycm + lo;
       WalkHit h;
       bool done = false;
-      uint64_t base = 0;
-      if (!walk_round<1, true>(ye, yc, ncp, A.Sy, base, lane, h, d.old_eff, &done) && !done &&
-          !walk_round<2, true>(ye, yc, ncp, A.Sy, base, lane, h, d.old_eff, &done) && !done)
-        while (base < A.Sy && !done && !walk_round<WU, true>(ye, yc, ncp, A.Sy, base, lane, h, d.old_eff, &done)) {
+      uint32_t base = 0;
+      const uint32_t Sy = (uint32_t)A.Sy;
+      if (!walk_round<1, true>(ye, yc, ncp, Sy, base, lane, h, d.old_eff, &done) && !done &&
+          !walk_round<2, true>(ye, yc, ncp, Sy, base, lane, h, d.old_eff, &done) && !done)
+        while (base < Sy && !done && !walk_round<WU, true>(ye, yc, ncp, Sy, base, lane, h, d.old_eff, &done)) {
         }
       if (lane == 0) *walked += base;
       r.eff = d.old_eff;
@@ -396,13 +397,13 @@ __device__ PairOut pair_argmax(const WalkArgs& A, int v, int p, uint64_t cpred, 
     const uint64_t ro = (uint64_t)(uint32_t)v * A.Sw32;
     const double* re = A.seff + ro;
     const uint64_t* rc = A.scm + ro;
-    const uint64_t S = A.S;
-    const uint64_t lim =
-        p <= A.pc ? (uint64_t)A.wbud * (A.pst_off[p + 1] - A.pst_off[p]) : S;
+    const uint32_t S = A.S32;
+    const uint32_t lim =
+        p <= A.pc ? (uint32_t)min((uint64_t)S, (uint64_t)A.wbud * (A.pst_off[p + 1] - A.pst_off[p])) : S;
     WalkHit h;
     // Rounds grow 32, 64, 128, then 32 * WU entries: most first admissible
     // entries sit in the first 32, deep walks still get WU loads per lane in flight.
-    uint64_t base = 0;
+    uint32_t base = 0;
     if (walk_round<1>(re, rc, ncp, S, base, lane, h) || walk_round<2>(re, rc, ncp, S, base, lane, h) ||
         walk_round<4>(re, rc, ncp, S, base, lane, h)) {
     } else {
