@@ -558,7 +558,7 @@ struct TeamState {
   uint8_t pd[64];                  // pair -> delta rescan eligible (P' = P - X + Y)
   uint64_t pc[64];                 // pair -> candidate predecessor mask
   uint64_t pm[64];                 // proposed graph (parent node masks by node)
-  double pb[64];                   // proposed per-node bests
+  alignas(16) double pb[64];       // proposed per-node bests
   uint64_t cm[64];                 // current graph
   double cb[64];                   // current per-node bests
   uint64_t tied, tied_new, rng, arng;
@@ -729,16 +729,31 @@ __global__ void __launch_bounds__(walk_cta_threads<TW>(), TW == 1 ? kWalkMinBloc
     pairs += np;
     team_sync<TW>(team);
     // ---- total in ascending node order (engine.cpp:95-96), tie bits, mh_accept
-    if (ttid == 0) {
-      double tot = 0.0;
-      for (int i = 0; i < n; ++i) tot += S.pb[i];
-      S.total = tot;
-      uint64_t tn = S.tied;
-      for (int q = 0; q < np; ++q) {
+    if (twarp == 0) {
+      // tie bits of the rescanned rows (distinct nodes: order-free), by the warp
+      uint64_t clr = 0, set = 0;
+      BNMC_FOR_NODES(q, lane, 32, np) {
         const uint64_t b = 1ull << S.pv[q];
-        tn = S.pt[q] ? (tn | b) : (tn & ~b);
+        clr |= b;
+        set |= S.pt[q] ? b : 0ull;
       }
-      S.tied_new = tn;
+      clr = ((uint64_t)__reduce_or_sync(0xffffffffu, (unsigned)(clr >> 32)) << 32) |
+            __reduce_or_sync(0xffffffffu, (unsigned)clr);
+      set = ((uint64_t)__reduce_or_sync(0xffffffffu, (unsigned)(set >> 32)) << 32) |
+            __reduce_or_sync(0xffffffffu, (unsigned)set);
+      if (lane == 0) S.tied_new = (S.tied & ~clr) | set;
+    }
+    if (ttid == 0) {
+      // serial sum in ascending node order (bit-exact), two values per load
+      double tot = 0.0;
+      const double2* pb2 = reinterpret_cast<const double2*>(S.pb);
+      for (int i = 0; i < (n >> 1); ++i) {
+        const double2 x = pb2[i];
+        tot += x.x;
+        tot += x.y;
+      }
+      if (n & 1) tot += S.pb[n - 1];
+      S.total = tot;
       // mh_accept, sampler.cpp:54-56: log10(u) < new - old
       const double delta = tot - S.cur_total;
       bool acc = t == 0 || thr_t < delta;
@@ -827,7 +842,7 @@ struct SpecSlot {
   uint8_t pv[64], pp[64], pt[64], pd[64];
   uint64_t pc[64];
   uint64_t pm[64];
-  double pb[64];
+  alignas(16) double pb[64];
   uint64_t rng_after, arng_after;
   double thr, total;
   int a, b, np, first;  // first: index of this slot's first pair in the flat list
@@ -1012,8 +1027,14 @@ __global__ void __launch_bounds__(1024, 1) walk_spec_kernel(WalkArgs A) {
     if (warp < d && lane == 0) {
       SpecSlot& S = s_sl[warp];
       const uint64_t it = t + warp;
-      double tot = 0.0;  // ascending node order, engine.cpp:95-96
-      for (int j = 0; j < n; ++j) tot += S.pb[j];
+      double tot = 0.0;  // ascending node order, engine.cpp:95-96 (two values per load)
+      const double2* pb2 = reinterpret_cast<const double2*>(S.pb);
+      for (int j = 0; j < (n >> 1); ++j) {
+        const double2 x = pb2[j];
+        tot += x.x;
+        tot += x.y;
+      }
+      if (n & 1) tot += S.pb[n - 1];
       S.total = tot;
       const double delta = tot - s_cur_total;
       S.acc = (uint8_t)(it == 0 || S.thr < delta);  // mh_accept, sampler.cpp:54-56
