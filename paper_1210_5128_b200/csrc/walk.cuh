@@ -267,6 +267,7 @@ struct PairOut {
   double eff;
   uint64_t cm;  // candidate mask of the chosen set
   int tied;     // another admissible set has exactly the same eff
+  uint32_t nw = 0, ne = 0;  // statistics: sorted entries walked, PST entries enumerated
 };
 
 // Warp-cooperative exact argmax of row v for the node at position p whose
@@ -352,10 +353,10 @@ struct DeltaIn {
 template <int EU, int WU>
 __device__ PairOut pair_argmax(const WalkArgs& A, int v, int p, uint64_t cpred, const uint8_t* order,
                                const uint8_t* ppos, const uint64_t* bt, const uint64_t* boff,
-                               const DeltaIn& d, unsigned long long* walked,
-                               unsigned long long* enumerated) {
+                               const DeltaIn& d) {
   const int lane = threadIdx.x & 31;
   PairOut r;
+  uint32_t walked_n = 0;
   if (p > A.pe) {
     const uint64_t ncp = ~cpred;
     if (d.on && A.yeff) {
@@ -374,7 +375,7 @@ __device__ PairOut pair_argmax(const WalkArgs& A, int v, int p, uint64_t cpred, 
           !walk_round<2, true>(ye, yc, ncp, Sy, base, lane, h, d.old_eff, &done) && !done)
         while (base < Sy && !done && !walk_round<WU, true>(ye, yc, ncp, Sy, base, lane, h, d.old_eff, &done)) {
         }
-      if (lane == 0) *walked += base;
+      r.nw = base;
       r.eff = d.old_eff;
       r.cm = d.old_cm;
       r.tied = 0;
@@ -410,8 +411,9 @@ __device__ PairOut pair_argmax(const WalkArgs& A, int v, int p, uint64_t cpred, 
       while (base < lim && base < S && !walk_round<WU>(re, rc, ncp, S, base, lane, h)) {
       }
     }
-    if (lane == 0) *walked += base;
+    walked_n = base;
     if (h.start != ~0ull) {
+      r.nw = base;
       r.eff = h.kstar;
       r.cm = h.kcm;
       r.tied = 0;
@@ -439,7 +441,8 @@ __device__ PairOut pair_argmax(const WalkArgs& A, int v, int p, uint64_t cpred, 
   const uint64_t* pst = de ? A.pst2 + A.pst2_off[p - 1] : A.pst + A.pst_off[p];
   const uint32_t cnt = de ? A.pst2_off[p] - A.pst2_off[p - 1] : A.pst_off[p + 1] - A.pst_off[p];
   r = enum_pst<EU>(A, v, pst, cnt, de ? d.ypos : -1, order, bt, boff);
-  if (lane == 0) *enumerated += cnt;
+  r.nw = walked_n;
+  r.ne = cnt;
   if (de) {
     if (!(r.eff >= d.old_eff)) {  // also covers cnt == 0 (s == 0)
       r.eff = d.old_eff;
@@ -583,14 +586,12 @@ __global__ void __launch_bounds__(walk_cta_threads<TW>(), TW == 1 ? kWalkMinBloc
   constexpr int kTeams = kCta / (32 * TW);
   __shared__ uint64_t s_bt[65 * 9];
   __shared__ uint64_t s_boff[9];  // size-class offsets of global_index for c = n - 1
-  __shared__ unsigned long long s_stat[kCta / 32][2];  // per warp: walked, enumerated
   __shared__ TeamState s_team[kTeams];
   const int tid = threadIdx.x, lane = tid & 31;
   const int team = (tid >> 5) / TW, twarp = (tid >> 5) % TW, ttid = tid - team * TW * 32;
   const int c = blockIdx.x * kTeams + team;
   const int n = A.n;
   for (int i = tid; i < 65 * 9; i += kCta) s_bt[i] = binom(i / 9, i % 9);
-  if (tid < 2 * (kCta / 32)) (&s_stat[0][0])[tid] = 0;
   if (tid < 9) {
     uint64_t o = 0;
     for (int j = tid + 1; j <= A.s; ++j) o += binom(A.n - 1, j);
@@ -624,8 +625,7 @@ __global__ void __launch_bounds__(walk_cta_threads<TW>(), TW == 1 ? kWalkMinBloc
     S.cur_total = 0.0;
   }
   team_sync<TW>(team);
-  unsigned long long* walked = &s_stat[tid >> 5][0];
-  unsigned long long* enumerated = &s_stat[tid >> 5][1];
+  unsigned long long walked = 0, enumerated = 0;  // statistics (lane 0 of each warp)
   unsigned long long pairs = 0;
   double thr_t = 0.0;
   const uint64_t T = score_only ? 0 : A.iters;
@@ -718,8 +718,9 @@ __global__ void __launch_bounds__(walk_cta_threads<TW>(), TW == 1 ? kWalkMinBloc
       d.old_eff = S.cb[v];
       d.old_cm = nodes_to_cand(S.cm[v], v);
       // few chains in flight (TW >= 8): more independent gathers per lane
-      const PairOut o = pair_argmax<TW >= 8 ? 4 : kEnumUnroll, TW >= 8 ? 8 : kWalkUnroll>(A, v, S.pp[q], S.pc[q], S.prop, S.ppos, s_bt, s_boff, d,
-                                    walked, enumerated);
+      const PairOut o = pair_argmax<TW >= 8 ? 4 : kEnumUnroll, TW >= 8 ? 8 : kWalkUnroll>(A, v, S.pp[q], S.pc[q], S.prop, S.ppos, s_bt, s_boff, d);
+      walked += o.nw;
+      enumerated += o.ne;
       if (lane == 0) {
         S.pm[v] = cand_to_nodes(o.cm, v);
         S.pb[v] = o.eff;
@@ -813,8 +814,8 @@ __global__ void __launch_bounds__(walk_cta_threads<TW>(), TW == 1 ? kWalkMinBloc
     }
   }
   if (lane == 0 && A.stat) {
-    atomicAdd(A.stat + 1, *walked);
-    atomicAdd(A.stat + 2, *enumerated);
+    atomicAdd(A.stat + 1, walked);
+    atomicAdd(A.stat + 2, enumerated);
     if (twarp == 0) atomicAdd(A.stat, pairs);
   }
 }
@@ -853,7 +854,6 @@ __global__ void __launch_bounds__(1024, 1) walk_spec_kernel(WalkArgs A) {
   constexpr int kThreads = 1024, kWarps = kThreads / 32;
   __shared__ uint64_t s_bt[65 * 9];
   __shared__ uint64_t s_boff[9];
-  __shared__ unsigned long long s_stat[kWarps][2];
   __shared__ SpecSlot s_sl[kSpecD];
   __shared__ uint8_t s_order[64];
   __shared__ uint64_t s_cm[64];
@@ -872,7 +872,6 @@ __global__ void __launch_bounds__(1024, 1) walk_spec_kernel(WalkArgs A) {
     for (int j = tid + 1; j <= A.s; ++j) o += binom(A.n - 1, j);
     s_boff[tid] = o;
   }
-  if (tid < 2 * kWarps) (&s_stat[0][0])[tid] = 0;
   if (tid == 0) {
     const Rng master{A.seeds[c]};
     Rng init = master.split(1);  // initial order: shuffle (sampler.cpp:83-86)
@@ -898,8 +897,7 @@ __global__ void __launch_bounds__(1024, 1) walk_spec_kernel(WalkArgs A) {
     s_cur_total = 0.0;
   }
   __syncthreads();
-  unsigned long long* walked = &s_stat[warp][0];
-  unsigned long long* enumerated = &s_stat[warp][1];
+  unsigned long long walked = 0, enumerated = 0;  // statistics (lane 0 of each warp)
   unsigned long long pairs = 0;
   uint64_t t = 0;  // iterations committed so far (0 = initial order not yet scored)
   while (t <= A.iters) {
@@ -1013,8 +1011,9 @@ __global__ void __launch_bounds__(1024, 1) walk_spec_kernel(WalkArgs A) {
       dl.ynode = S.prop[lo];
       dl.old_eff = s_cb[v];
       dl.old_cm = nodes_to_cand(s_cm[v], v);
-      const PairOut o = pair_argmax<4, 8>(A, v, S.pp[qi], S.pc[qi], S.prop, S.ppos, s_bt, s_boff, dl,
-                                          walked, enumerated);
+      const PairOut o = pair_argmax<4, 8>(A, v, S.pp[qi], S.pc[qi], S.prop, S.ppos, s_bt, s_boff, dl);
+      walked += o.nw;
+      enumerated += o.ne;
       if (lane == 0) {
         S.pm[v] = cand_to_nodes(o.cm, v);
         S.pb[v] = o.eff;
@@ -1104,8 +1103,8 @@ __global__ void __launch_bounds__(1024, 1) walk_spec_kernel(WalkArgs A) {
     if (A.stat) atomicAdd(A.stat, pairs);
   }
   if (lane == 0 && A.stat) {
-    atomicAdd(A.stat + 1, *walked);
-    atomicAdd(A.stat + 2, *enumerated);
+    atomicAdd(A.stat + 1, walked);
+    atomicAdd(A.stat + 2, enumerated);
   }
 }
 
