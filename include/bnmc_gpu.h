@@ -196,8 +196,10 @@ int bnmc_gpu_table_set_walk_params(bnmc_table* t, int64_t enum_max, int ylists);
  * enum_max < S(p,s) <= walk_cap walk at most budget * S(p,s) sorted entries
  * and then enumerate PST(p) (bounds the deep walks of rows with few
  * predecessors). walk_cap < 0: default S(n-1,s) / 512; budget < 0: default
- * 16; budget 0 disables the cap. */
-int bnmc_gpu_table_set_walk_cap(bnmc_table* t, int64_t walk_cap, int64_t budget);
+ * 16; budget 0 disables the cap. deep: entries per lane per deep walk round
+ * for chains of fewer than 8 warps, -1 auto (8 for rows longer than 2^21
+ * entries, else 4), 0 -> 4, 1 -> 8. */
+int bnmc_gpu_table_set_walk_cap(bnmc_table* t, int64_t walk_cap, int64_t budget, int deep);
 
 /* Statistics of the last sorted-walk run_chains call: (chain, row) pairs
  * rescanned, sorted entries walked, PST entries enumerated (small predecessor

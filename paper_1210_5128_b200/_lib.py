@@ -71,7 +71,7 @@ SIGNATURES = {
     "bnmc_gpu_last_walk_stats": (C.c_int, [_vp, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64),
                                            C.POINTER(C.c_uint64), C.POINTER(C.c_float)]),
     "bnmc_gpu_table_set_walk_params": (C.c_int, [_vp, C.c_int64, C.c_int]),
-    "bnmc_gpu_table_set_walk_cap": (C.c_int, [_vp, C.c_int64, C.c_int64]),
+    "bnmc_gpu_table_set_walk_cap": (C.c_int, [_vp, C.c_int64, C.c_int64, C.c_int]),
     "bnmc_gpu_last_replayed": (C.c_int, [_vp, C.POINTER(C.c_uint64)]),
     "bnmc_gpu_bench_scan": (C.c_int, [_vp, _i32p, C.c_int, C.c_int, C.c_int, C.c_int,
                                       C.POINTER(C.c_float)]),

@@ -183,6 +183,7 @@ struct bnmc_table {
   uint64_t enum_max = kEnumMax;  // enumerate rows with S(p,s) <= enum_max, walk the others
   uint64_t walk_cap = env_u64("BNMC_WALK_CAP", 0);  // 0: S(n-1,s) / kWalkCapDiv
   uint32_t walk_budget = static_cast<uint32_t>(env_u64("BNMC_WALK_BUDGET", kWalkBudget));
+  int walk_deep = -1;  // 8 entries per lane per deep walk round: -1 auto (long rows), 0 off, 1 on
   int scan_mode = 0;  // default for score_orders: 0 auto (walk), 1 full-row scan
   DevBuf<int> d_fo, d_tc;
   DevBuf<unsigned long long> d_acc;
@@ -664,13 +665,24 @@ void launch_walk(bnmc_table* t, const WalkArgs& A, int C, int team_warps = 0) {
     t->last_team = 32;
     return;
   }
+  // deep rows (long walks): 8 entries per lane per round for small teams
+  const bool deep = t->walk_deep < 0 ? t->S > kDeepRowEntries : t->walk_deep == 1;
   switch (tw) {
     case 32: walk_chain_kernel<32><<<grid, cta, 0, t->stream>>>(A); break;
     case 16: walk_chain_kernel<16><<<grid, cta, 0, t->stream>>>(A); break;
     case 8: walk_chain_kernel<8><<<grid, cta, 0, t->stream>>>(A); break;
-    case 4: walk_chain_kernel<4><<<grid, cta, 0, t->stream>>>(A); break;
-    case 2: walk_chain_kernel<2><<<grid, cta, 0, t->stream>>>(A); break;
-    case 1: walk_chain_kernel<1><<<grid, cta, 0, t->stream>>>(A); break;
+    case 4:
+      if (deep) walk_chain_kernel<4, 8><<<grid, cta, 0, t->stream>>>(A);
+      else walk_chain_kernel<4><<<grid, cta, 0, t->stream>>>(A);
+      break;
+    case 2:
+      if (deep) walk_chain_kernel<2, 8><<<grid, cta, 0, t->stream>>>(A);
+      else walk_chain_kernel<2><<<grid, cta, 0, t->stream>>>(A);
+      break;
+    case 1:
+      if (deep) walk_chain_kernel<1, 8><<<grid, cta, 0, t->stream>>>(A);
+      else walk_chain_kernel<1><<<grid, cta, 0, t->stream>>>(A);
+      break;
     default: raise(BNMC_USAGE, "team_warps must be 0, 1, 2, 4, 8, 16 or 32");
   }
   CK(cudaGetLastError());
@@ -1424,9 +1436,11 @@ int bnmc_gpu_table_set_scan_mode(bnmc_table* t, int mode) {
   });
 }
 
-int bnmc_gpu_table_set_walk_cap(bnmc_table* t, int64_t walk_cap, int64_t budget) {
+int bnmc_gpu_table_set_walk_cap(bnmc_table* t, int64_t walk_cap, int64_t budget, int deep) {
   return guarded([&] {
     if (!t) raise(BNMC_USAGE, "null table");
+    if (deep < -1 || deep > 1) raise(BNMC_USAGE, "deep must be -1, 0 or 1");
+    t->walk_deep = deep;
     if (budget > 0xFFFF) raise(BNMC_USAGE, "walk budget must be <= 65535");
     t->walk_cap = walk_cap < 0 ? 0 : static_cast<uint64_t>(walk_cap);
     t->walk_budget = budget < 0 ? static_cast<uint32_t>(kWalkBudget) : static_cast<uint32_t>(budget);

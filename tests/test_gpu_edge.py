@@ -288,10 +288,10 @@ def test_device_acceptance_and_exact_replay():
     np.testing.assert_array_equal(ref_b.trace_proposed[7], o["trace_proposed"])
 
 
-@pytest.mark.parametrize("enum_max,ylists,cap,budget", [
-    (0, 1, -1, 0), (0, 0, -1, 0), (-1, 1, -1, -1), (1 << 40, 0, -1, -1),
-    (0, 1, 1 << 40, 1), (0, 0, 1 << 40, 1), (-1, 1, 1 << 40, 2)])
-def test_walk_tuning_paths_identical(enum_max, ylists, cap, budget):
+@pytest.mark.parametrize("enum_max,ylists,cap,budget,deep", [
+    (0, 1, -1, 0, -1), (0, 0, -1, 0, 1), (-1, 1, -1, -1, -1), (1 << 40, 0, -1, -1, 0),
+    (0, 1, 1 << 40, 1, 1), (0, 0, 1 << 40, 1, 0), (-1, 1, 1 << 40, 2, 1)])
+def test_walk_tuning_paths_identical(enum_max, ylists, cap, budget, deep):
     """Every walk-path variant — all rows walked (with / without the delta-walk
     lists), default split, all rows enumerated, capped walks that fall back to
     enumeration for nearly every row — on tie-heavy and ordinary instances
@@ -299,10 +299,11 @@ def test_walk_tuning_paths_identical(enum_max, ylists, cap, budget):
     import ctypes as C
     for cells, cards, s, gamma in (rand_instance(21, 14, 3, cmax=2) + (3, 1.0),
                                    rand_instance(23, 16, 400) + (3, 0.2)):
-        cfg = P.RunConfig(max_parents=s, gamma=gamma, iterations=200, scan_mode=2)
+        # one warp per chain: the team size whose deep-round width `deep` selects
+        cfg = P.RunConfig(max_parents=s, gamma=gamma, iterations=200, scan_mode=2, team_warps=1)
         cache = P.ScoreCache.build(P.Dataset(cards, cells), cfg)
         _lib.check(_lib.lib().bnmc_gpu_table_set_walk_params(cache.handle, enum_max, ylists))
-        _lib.check(_lib.lib().bnmc_gpu_table_set_walk_cap(cache.handle, cap, budget))
+        _lib.check(_lib.lib().bnmc_gpu_table_set_walk_cap(cache.handle, cap, budget, deep))
         t = port.cache_build(cells, cards, s, gamma, 1.0)
         rs = P.run_chains(cache, None, [1, 2, 3], cfg)
         for c, seed in enumerate([1, 2, 3]):
