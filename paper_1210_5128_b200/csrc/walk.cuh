@@ -19,13 +19,19 @@
 //     (combinatorics.hpp:83-101): position subset -> node mask -> cache index
 //     (index_of / global_index) -> exact eff; strict '>' per lane and a
 //     (value desc, index asc) reduction reproduce scan_slice + argmax_reduce
-//     exactly.
-//   * One CTA runs one chain for all its iterations (run_mcmc loop body,
-//     sampler.cpp:92-111): propose_swap from the split(2) stream, rescan of the
-//     rows whose predecessor sets changed (positions min(a,b)..max(a,b), plus
-//     rows whose best is an exact tie), total in ascending node order,
-//     mh_accept against the host's glibc log10(u_t), BestGraphTracker::update,
-//     trace row. No per-iteration launch, no host round trip.
+//     exactly. Rows with kEnumMax < S(p,s) <= S/512 walk at most 16 S(p,s)
+//     entries and then enumerate (capped walks).
+//   * Middle rows of a swap whose best avoids the node that moved later
+//     (P' = P - X + Y) walk only the per-(row, Y) list of sorted entries
+//     containing Y, down to the current best's value (delta walks).
+//   * A team of TW warps runs one chain for all its iterations (run_mcmc loop
+//     body, sampler.cpp:92-111): propose_swap from the split(2) stream, rescan
+//     of the rows whose predecessor sets changed (positions min(a,b)..max(a,b),
+//     plus rows whose best is an exact tie), total in ascending node order,
+//     mh_accept (device log10 with a host replay when within 2^-48 of the
+//     threshold), BestGraphTracker::update, trace row. No per-iteration launch,
+//     no host round trip. walk_spec_kernel: one chain per 1024-thread CTA
+//     evaluating kSpecD proposals per round.
 #pragma once
 
 #include "chain.cuh"
