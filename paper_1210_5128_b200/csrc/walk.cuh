@@ -376,6 +376,12 @@ __device__ PairOut pair_argmax(const WalkArgs& A, int v, int p, uint64_t cpred, 
       const uint64_t lo = (uint64_t)(uint32_t)(v * (A.n - 1) + qy) * A.Syw32;
       const double* ye = A.yeff + lo;
       const uint64_t* yc = A.ycm + lo;
+      r.eff = d.old_eff;
+      r.cm = d.old_cm;
+      r.tied = 0;
+      // the list's head is the best set containing Y (admissible or not):
+      // below the current best, nothing containing Y can change the row
+      if (__ldg(ye) < d.old_eff) return r;
       WalkHit h;
       bool done = false;
       uint32_t base = 0;
@@ -385,9 +391,6 @@ __device__ PairOut pair_argmax(const WalkArgs& A, int v, int p, uint64_t cpred, 
         while (base < Sy && !done && !walk_round<WU, true>(ye, yc, ncp, Sy, base, lane, h, d.old_eff, &done)) {
         }
       r.nw = base;
-      r.eff = d.old_eff;
-      r.cm = d.old_cm;
-      r.tied = 0;
       if (h.start == ~0ull) return r;  // no set containing Y reaches the current best
       int ties = 0;
       uint64_t cm = h.kcm;
