@@ -393,3 +393,17 @@ def test_speculative_single_chain_kernel(strict, tol, exact):
             o = port.run_mcmc(t2, 3, 1100, seed)
             np.testing.assert_array_equal(r2[c].trace_proposed, o["trace_proposed"])
             np.testing.assert_array_equal(r2[c].tracker_masks, o["tracker_masks"])
+
+
+def test_walk_cap_argument_errors():
+    """set_walk_cap validates its mode and budget (usage error, table unchanged)."""
+    cells, cards = rand_instance(5, 8, 50)
+    cfg = P.RunConfig(max_parents=2, iterations=20, scan_mode=2)
+    cache = P.ScoreCache.build(P.Dataset(cards, cells), cfg)
+    L = _lib.lib()
+    assert L.bnmc_gpu_table_set_walk_cap(cache.handle, -1, -1, 2) == 2
+    assert L.bnmc_gpu_table_set_walk_cap(cache.handle, -1, 1 << 20, -1) == 2
+    assert L.bnmc_gpu_table_set_walk_cap(cache.handle, -1, -1, -1) == 0
+    t = port.cache_build(cells, cards, 2, 0.1, 1.0)
+    r = P.run_chains(cache, None, [4], cfg)[0]
+    np.testing.assert_array_equal(r.trace_proposed, port.run_mcmc(t, 2, 20, 4)["trace_proposed"])

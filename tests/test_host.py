@@ -54,6 +54,15 @@ def test_pure_host_entry_points():
     assert L.bnmc_gpu_bounded_subset_count(63, 5) == 7666240
 
 
+def test_tuning_entry_points_reject_bad_arguments():
+    """Walk / scan tuning setters: usage errors (status 2) on a null table or
+    out-of-range values, without touching a device."""
+    L = _lib.lib()
+    assert L.bnmc_gpu_table_set_walk_cap(None, -1, -1, -1) == 2
+    assert L.bnmc_gpu_table_set_walk_params(None, -1, -1) == 2
+    assert L.bnmc_gpu_table_set_scan_mode(None, 0) == 2
+
+
 @pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg3", "cfg4"])
 def test_generator_is_reference_identical(name, golden_meta):
     data, pri, cfg, truth = P.baseline_instance(name)
