@@ -8,7 +8,8 @@ the way SURVEY §8d prescribes:
     OrderScorer::score on random orders (reference, all host threads) vs the
     device scan (masks and totals bit-exact);
   * a short chain: reference run_mcmc on the loaded cache vs the device chain
-    with the same seed (trace, tracker, final state bit-exact).
+    with the same seed (trace, tracker, final state bit-exact);
+  * 8 one-warp chains (deep-row walk rounds) vs whole-CTA chains, same seeds.
 Prints one JSON object (committed as profiles/r01_cfg5_parity.json).
   python tools/cfg5_parity.py [iterations] [orders]
 """
@@ -82,4 +83,14 @@ out["chain_tracker_bit_exact"] = bool(np.array_equal(ours.tracker_masks, r.track
 out["chain_final_state_equal"] = bool(np.array_equal(ours.final_order, r.final_order)
                                       and ours.final_score == r.final_score
                                       and ours.accepted == r.accepted)
+# one-warp chains (deep-row walk rounds, capped walks) vs whole-CTA chains for
+# the same seeds; seed 1 of the latter is the chain compared with the reference
+seeds = list(range(1, 9))
+cfg.scan_mode = 2
+cfg.team_warps = 1
+one = P.run_chains(cache, pri, seeds, cfg)
+cfg.team_warps = 32
+big = P.run_chains(cache, pri, seeds, cfg)
+out["one_warp_chains_equal_cta_chains"] = f"{sum(int(np.array_equal(a.trace_proposed, b.trace_proposed) and np.array_equal(a.tracker_masks, b.tracker_masks) and np.array_equal(a.final_order, b.final_order)) for a, b in zip(one, big))}/{len(seeds)}"
+out["cta_chain_seed1_equals_reference"] = bool(np.array_equal(big[0].trace_proposed, r.trace_proposed))
 print(json.dumps(out), flush=True)
