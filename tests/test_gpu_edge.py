@@ -407,3 +407,35 @@ def test_walk_cap_argument_errors():
     t = port.cache_build(cells, cards, 2, 0.1, 1.0)
     r = P.run_chains(cache, None, [4], cfg)[0]
     np.testing.assert_array_equal(r.trace_proposed, port.run_mcmc(t, 2, 20, 4)["trace_proposed"])
+
+
+def test_walk_variants_stress():
+    """Random instances (n up to 30, s up to 5, priors) through every walk
+    variant — team sizes 1/2/4/8/32, deep rounds off/on, capped walks off /
+    budget 1 / default — against the oracle's chains bit for bit.
+    BNMC_STRESS_TRIALS raises the instance count (default 8; 200 passed)."""
+    import os
+    trials = int(os.environ.get("BNMC_STRESS_TRIALS", "8"))
+    rng = np.random.default_rng(77)
+    L = _lib.lib()
+    for trial in range(trials):
+        n = int(rng.integers(8, 31))
+        s = int(rng.integers(1, 6))
+        m = int(rng.choice([30, 200, 1000]))
+        cells, cards = rand_instance(3000 + trial, n, m, cmax=int(rng.integers(2, 4)))
+        pri = np.where(rng.random((n, n)) < 0.2, rng.choice([0.1, 0.3, 0.7, 0.9], (n, n)), 0.5)
+        iters = 80
+        cfg = P.RunConfig(max_parents=s, iterations=iters, scan_mode=2)
+        cache = P.ScoreCache.build(P.Dataset(cards, cells), cfg, pri)
+        t = port.cache_build(cells, cards, s, 0.1, 1.0)
+        seeds = [trial * 7 + 1, trial * 7 + 2]
+        want = [port.run_mcmc(t, s, iters, sd, pri) for sd in seeds]
+        for tw, deep, budget in ((1, 0, -1), (1, 1, 1), (2, 1, 0), (4, 0, 1), (8, -1, -1),
+                                 (32, -1, 1)):
+            _lib.check(L.bnmc_gpu_table_set_walk_cap(cache.handle, -1, budget, deep))
+            cfg.team_warps = tw
+            rs = P.run_chains(cache, pri, seeds, cfg)
+            for r, o in zip(rs, want):
+                np.testing.assert_array_equal(r.trace_proposed, o["trace_proposed"])
+                np.testing.assert_array_equal(r.tracker_masks, o["tracker_masks"])
+                np.testing.assert_array_equal(r.final_order, o["final_order"])
