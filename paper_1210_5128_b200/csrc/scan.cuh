@@ -152,6 +152,10 @@ __global__ void __launch_bounds__(kScan2Threads, kScan2Per > 8 ? 2 : 4) scan2_ke
 #pragma unroll
     for (int e = 0; e < kScan2Per; ++e) inter &= m[e];
   }
+  // nodes common to every entry of the warp's 256 (lexicographically adjacent)
+  // sets: a pair whose predecessors miss one of them has nothing admissible here
+  const uint64_t winter = ((uint64_t)__reduce_and_sync(0xffffffffu, (unsigned)(inter >> 32)) << 32) |
+                          __reduce_and_sync(0xffffffffu, (unsigned)inter);
   for (int i = tid; i < kScan2MaxRows * kMaxChains * 2; i += kScan2Threads) (&s_cell[0][0][0])[i] = 0ull;
   cudaGridDependencySynchronize();
   if (tid == 0) s_sel = *a.sel;
@@ -215,6 +219,7 @@ __global__ void __launch_bounds__(kScan2Threads, kScan2Per > 8 ? 2 : 4) scan2_ke
     const int cnt = s_cnt[v];
     for (int q = 0; q < cnt; ++q) {
       const uint64_t ncp = ~a.buckets[(b * n + v) * kMaxChains + q].cpred;
+      if ((winter & ncp) != 0) continue;  // warp-uniform: no entry of the warp admissible
       // branch-free lane max: inadmissible entries become -inf (keys are finite)
       float kk[kScan2Per];
 #pragma unroll
