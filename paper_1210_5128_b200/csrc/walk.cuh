@@ -578,6 +578,7 @@ struct TeamState {
   double cb[64];                   // current per-node bests
   uint64_t tied, tied_new, rng, arng;
   double total, cur_total;
+  double tmin;  // tracker minimum when full (-inf before), kept by the insert path
   unsigned long long acc;
   int np, a, b, accept, tcount, amb;
 };
@@ -636,6 +637,7 @@ __global__ void __launch_bounds__(walk_cta_threads<TW>(), TW == 1 ? kWalkMinBloc
     S.tied = 0;
     S.amb = 0;
     S.tcount = 0;
+    S.tmin = -INFINITY;
     S.acc = 0;
     S.cur_total = 0.0;
   }
@@ -794,9 +796,15 @@ __global__ void __launch_bounds__(walk_cta_threads<TW>(), TW == 1 ? kWalkMinBloc
     const double proposed = S.total;
     const bool accepted = S.accept;
     // ---- BestGraphTracker::update; every proposal is offered unless strict
-    if (twarp == 0 && (t == 0 || accepted || !A.strict))
-      tracker_offer_warp<false>(A.tmasks + (uint64_t)c * A.K * n, A.ttotals + (uint64_t)c * A.K,
-                                A.thash + (uint64_t)c * A.K, A.K, n, S.pm, proposed, &S.tcount, nullptr);
+    // (the full tracker's minimum is mirrored in shared memory: the common
+    // rejection needs no global load)
+    if (twarp == 0 && (t == 0 || accepted || !A.strict) && !(S.tcount == A.K && proposed <= S.tmin)) {
+      double* tt = A.ttotals + (uint64_t)c * A.K;
+      tracker_insert_warp<false>(A.tmasks + (uint64_t)c * A.K * n, tt, A.thash + (uint64_t)c * A.K, A.K,
+                                 n, S.pm, proposed, &S.tcount, nullptr);
+      __syncwarp();
+      if (lane == 0 && S.tcount == A.K) S.tmin = tt[A.K - 1];
+    }
     // ---- commit + trace row
     if (accepted)
       for (int i = ttid; i < n; i += TW * 32) {
