@@ -117,6 +117,18 @@ def flush_l2(torch, buf):
     buf.add_(1.0)  # 256 MiB write > 126 MB L2
 
 
+def cpu_model():
+    """Host CPU model string (/proc/cpuinfo), reported with the CPU baseline."""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_baseline(cache, priors, cfg, ours_trace, iters, seed):
     """Reference run_mcmc (oracle/_ref) on the GPU-built table, all host threads."""
     from oracle import ref
@@ -134,7 +146,7 @@ def cpu_baseline(cache, priors, cfg, ours_trace, iters, seed):
     wall = time.perf_counter() - t0
     parity = bool(np.array_equal(r.trace_proposed, ours_trace[:iters]))
     return {"value": iters / r.sampling_seconds, "unit": "iterations/s",
-            "cores": ref.max_threads(), "kind": "reference",
+            "cores": ref.max_threads(), "cpu_model": cpu_model(), "kind": "reference",
             "sample": f"{iters} run_mcmc iterations (seed {seed}) of the unmodified reference "
                       f"(oracle/_ref, OpenMP {ref.max_threads()} threads) on the GPU-built table "
                       f"loaded via ScoreCache::load; wall {wall:.1f}s",
@@ -356,6 +368,7 @@ def run_reference(args):
            "config": {"workload": f"{args.config}: n=60 k=4 m=10000 3-state + pairwise priors; "
                                   f"1 chain x {I} iterations per step"},
            "cpu_baseline": {"value": value, "unit": "iterations/s", "cores": ref.max_threads(),
+                            "cpu_model": cpu_model(),
                             "kind": "reference", "sample": sample},
            "e2e": {"value": value, "unit": "iterations/s", "h2d_bytes_per_step": 0,
                    "d2h_bytes_per_step": 0}}
