@@ -129,16 +129,56 @@ def cpu_model():
     return "unknown"
 
 
-def cpu_baseline(cache, priors, cfg, ours_trace, iters, seed):
-    """Reference run_mcmc (oracle/_ref) on the GPU-built table, all host threads."""
+def reference_cache(cache, cfg):
+    """The reference's ScoreCache::load of the GPU-built table (BNSC export)."""
     from oracle import ref
     if not ref.available():
         return None
-    n, s = cache.n(), cache.s()
-    with tempfile.TemporaryDirectory() as d:
+    tmp = "/dev/shm" if os.path.isdir("/dev/shm") else None
+    with tempfile.TemporaryDirectory(dir=tmp) as d:
         path = os.path.join(d, "cfg.bnsc")
         cache.save(path)
-        rc = ref.Cache.load(path, s, cfg.gamma, cfg.ess, False)
+        return ref.Cache.load(path, cache.s(), cfg.gamma, cfg.ess, False)
+
+
+def headline_parity(rc, out, seeds, priors, n, s, iters, count, team=8):
+    """Chains of the LAST timed launch (18,944 chains, the headline kernel
+    variant) compared bit-for-bit with the unmodified reference's run_mcmc
+    (oracle/_ref, sampler.cpp:58-116) on the same table: full traces
+    (proposed, accepted, best), trackers (masks, totals), final order, final
+    score, accepted count. Chains are spread over CTAs and warp slots."""
+    from oracle import ref
+    C_ = len(seeds)
+    idx = sorted({min(C_ - 1, (k * C_) // count + (k % team)) for k in range(count)})
+    dummy = np.zeros((1, n), np.uint8)  # run_mcmc needs rows > 0; prebuilt skips the build
+    cards = np.full(n, 3, np.int32)
+    ok, bad, t0 = 0, [], time.perf_counter()
+    for c in idx:
+        r = ref.run_mcmc(dummy, cards, s, iters, int(seeds[c]), priors=priors, prebuilt=rc)
+        k = int(out.tracker_count[c])
+        same = (np.array_equal(out.trace_proposed[c].view(np.uint64), r.trace_proposed.view(np.uint64))
+                and np.array_equal(out.trace_accepted[c].astype(bool), r.trace_accepted)
+                and np.array_equal(out.trace_best[c].view(np.uint64), r.trace_best.view(np.uint64))
+                and k == r.tracker_totals.size
+                and np.array_equal(out.tracker_masks[c, :k], r.tracker_masks)
+                and np.array_equal(out.tracker_totals[c, :k].view(np.uint64),
+                                   r.tracker_totals.view(np.uint64))
+                and np.array_equal(out.final_order[c], r.final_order)
+                and float(out.final_score[c]) == r.final_score
+                and int(out.accepted[c]) == r.accepted)
+        ok += int(same)
+        if not same:
+            bad.append(c)
+    return {"parity_checked_chains": f"{ok}/{len(idx)}", "chain_indices": idx,
+            "iterations": iters, "mismatched": bad, "reference_seconds": time.perf_counter() - t0,
+            "against": "oracle/_ref run_mcmc (unmodified reference) on the GPU-built table"}
+
+
+def cpu_baseline(rc, n, s, priors, ours_trace, iters, seed):
+    """Reference run_mcmc (oracle/_ref) on the GPU-built table, all host threads."""
+    from oracle import ref
+    if rc is None:
+        return None
     dummy = np.zeros((1, n), np.uint8)  # run_mcmc needs rows > 0; prebuilt skips the build
     cards = np.full(n, 3, np.int32)
     t0 = time.perf_counter()
@@ -266,11 +306,18 @@ def run_ours(args):
         best = D.best_overall(allrec, n)
         cpu = None
         extra = {}
-        if world == 1 and not args.no_cpu_baseline:
+        rc = None
+        if world == 1 and not (args.no_cpu_baseline and args.parity_chains == 0):
+            rc = reference_cache(cache, cfg)
+        if rc is not None and args.parity_chains > 0:
+            extra["headline_parity"] = headline_parity(
+                rc, out, D.chain_seeds(1, rank, Cn, args.steps - 1, world), pri, n,
+                cfg.max_parents, I, args.parity_chains)
+        if rc is not None and not args.no_cpu_baseline:
             c1 = P.RunConfig(max_parents=cfg.max_parents, iterations=args.cpu_iters, seed=1,
                              memory_cap_bytes=cfg.memory_cap_bytes, device=local, scan_mode=2)
             ours1 = P.run_chains(cache, pri, [1], c1)[0]
-            cpu = cpu_baseline(cache, pri, cfg, ours1.trace_proposed, args.cpu_iters, 1)
+            cpu = cpu_baseline(rc, n, cfg.max_parents, pri, ours1.trace_proposed, args.cpu_iters, 1)
         if world == 1 and not args.no_extras:
             # one chain (the reference's own unit of work): latency-bound, the
             # speculative single-chain kernel runs at >= 1000 iterations
@@ -390,6 +437,8 @@ def main():
                     help="run the multi-GPU code path (NCCL) even at world size 1")
     ap.add_argument("--iters", type=int, default=500, help="MCMC iterations per chain per step")
     ap.add_argument("--cpu-iters", type=int, default=200)
+    ap.add_argument("--parity-chains", type=int, default=16,
+                    help="chains of the last timed launch checked against oracle/_ref (0 off)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-iters", type=int, default=30)
     ap.add_argument("--ref-rows", type=int, default=1000)

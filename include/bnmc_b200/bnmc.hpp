@@ -20,9 +20,10 @@
 //   * ScoreCache copies share one device table (the table is immutable after
 //     build, so value semantics are preserved); at()/lookup() read a host
 //     mirror downloaded on first use.
-//   * RunConfig::debug_recheck rescores the final order with score_order and
-//     throws bnmc::Error on drift (the reference checks every 100 iterations;
-//     the device loop is not interrupted).
+//   * RunConfig::debug_recheck re-scores every chain's current order from
+//     scratch on the device every 100 iterations (sampler.cpp:105-110) and
+//     throws bnmc::Error("chain score drifted from recomputation at iteration
+//     N") on a difference, like the reference.
 //   * Extensions: RunConfig::device (CUDA ordinal), ScoreCache::upload /
 //     device_table(), OrderScorer::score_many, run_chains (independent chains
 //     in one device launch).

@@ -156,6 +156,11 @@ typedef struct {
                           decision inside the CUDA/glibc log10 error bound replayed
                           with host glibc thresholds; 1 = host glibc thresholds only */
   int accept_tol_log2; /* relative bound of that test as a power of two (0 = -48) */
+  int debug_recheck;   /* RunConfig::debug_recheck (sampler.cpp:105-110): every 100
+                          iterations each chain re-scores its current order from
+                          scratch (full rows, no incremental state) on the device
+                          and fails with status 1 ("chain score drifted ...") when
+                          the total differs; sorted-walk path only */
 } bnmc_chain_params;
 
 /* Run n_chains independent chains, chain c seeded with seeds[c] exactly as
@@ -206,6 +211,12 @@ int bnmc_gpu_table_set_walk_cap(bnmc_table* t, int64_t walk_cap, int64_t budget,
  * counts), and the device time of the last per-row sort build (ms). */
 int bnmc_gpu_last_walk_stats(const bnmc_table* t, uint64_t* pairs, uint64_t* walked,
                              uint64_t* enumerated, float* sort_ms);
+
+/* Kernel variant of the last sorted-walk launch (run_chains or score_orders):
+ * warps per chain, entries per lane in a deep walk round (4 or 8), and
+ * whether the speculative single-chain kernel ran (walk_spec_kernel). */
+int bnmc_gpu_last_walk_variant(const bnmc_table* t, int* team_warps, int* entries_per_lane,
+                               int* speculative);
 
 /* Chains of the last sorted-walk run_chains call that were replayed with host
  * glibc acceptance thresholds (an mh_accept decision fell inside the bound). */

@@ -31,7 +31,8 @@ class ScoreParams(C.Structure):
 class ChainParams(C.Structure):
     _fields_ = [("iterations", C.c_uint64), ("track_top", C.c_int), ("strict", C.c_int),
                 ("scan_mode", C.c_int), ("timing_sample", C.c_int), ("team_warps", C.c_int),
-                ("exact_accept", C.c_int), ("accept_tol_log2", C.c_int)]
+                ("exact_accept", C.c_int), ("accept_tol_log2", C.c_int),
+                ("debug_recheck", C.c_int)]
 
 
 # Every exported symbol with its ctypes signature: (restype, argtypes).
@@ -73,6 +74,8 @@ SIGNATURES = {
     "bnmc_gpu_table_set_walk_params": (C.c_int, [_vp, C.c_int64, C.c_int]),
     "bnmc_gpu_table_set_walk_cap": (C.c_int, [_vp, C.c_int64, C.c_int64, C.c_int]),
     "bnmc_gpu_last_replayed": (C.c_int, [_vp, C.POINTER(C.c_uint64)]),
+    "bnmc_gpu_last_walk_variant": (C.c_int, [_vp, C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                             C.POINTER(C.c_int)]),
     "bnmc_gpu_bench_scan": (C.c_int, [_vp, _i32p, C.c_int, C.c_int, C.c_int, C.c_int,
                                       C.POINTER(C.c_float)]),
     "bnmc_synth_last_error": (C.c_char_p, []),

@@ -344,6 +344,21 @@ class ScoreCache:
             _lib.check(_lib.lib().bnmc_gpu_table_set_priors(self._h, _lib.ptr(pr)))
             self._priors_key = key
 
+    def last_walk_stats(self):
+        """Statistics and kernel variant of the last sorted-walk launch on this table."""
+        L = _lib.lib()
+        pa, wa, en, so = C.c_uint64(), C.c_uint64(), C.c_uint64(), C.c_float()
+        _lib.check(L.bnmc_gpu_last_walk_stats(self._h, C.byref(pa), C.byref(wa), C.byref(en),
+                                              C.byref(so)))
+        tw, wu, sp, rp = C.c_int(), C.c_int(), C.c_int(), C.c_uint64()
+        _lib.check(L.bnmc_gpu_last_walk_variant(self._h, C.byref(tw), C.byref(wu), C.byref(sp)))
+        _lib.check(L.bnmc_gpu_last_replayed(self._h, C.byref(rp)))
+        return {"pairs": pa.value, "walked": wa.value, "enumerated": en.value,
+                "sort_ms": so.value, "team_warps": tw.value, "entries_per_lane": wu.value,
+                "speculative": bool(sp.value), "replayed": rp.value,
+                "variant": "walk_spec_kernel" if sp.value else
+                           f"walk_chain_kernel<{tw.value},{wu.value}>"}
+
     @property
     def handle(self):
         return self._h
@@ -505,7 +520,8 @@ def run_chains_batch(cache: ScoreCache, priors, seeds, cfg: RunConfig, out: Chai
                          np.empty((nc, K)), 0.0, 0.0)
     ms = C.c_float()
     params = _lib.ChainParams(it, K, int(cfg.strict_paper_tracker), cfg.scan_mode, 0,
-                              cfg.team_warps, cfg.exact_accept, cfg.accept_tol_log2)
+                              cfg.team_warps, cfg.exact_accept, cfg.accept_tol_log2,
+                              int(cfg.debug_recheck))
     t0 = time.perf_counter()
     _lib.check(_lib.lib().bnmc_gpu_run_chains(
         cache.handle, seeds, nc, C.byref(params), _lib.ptr(out.trace_proposed),

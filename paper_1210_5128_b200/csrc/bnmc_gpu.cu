@@ -211,8 +211,9 @@ struct bnmc_table {
   DevBuf<double> out_best, out_total;
   uint64_t last_rescans = 0, last_sectors = 0, last_launches = 0, last_scan_samples = 0;
   uint64_t last_walked = 0, last_enumerated = 0;
-  int last_team = 0;
+  int last_team = 0, last_wu = 0, last_spec = 0;
   uint64_t last_replayed = 0;
+  uint64_t last_drift_it = 0;  // debug_recheck: first iteration whose rescore differed
   DevBuf<int> d_amb;
   float last_scan_ms = 0.f, last_total_ms = 0.f;
   int last_G = 0;
@@ -577,11 +578,13 @@ void build_pst_small(bnmc_table* t) {
 // Sorted rows (descending eff, CUB radix sort per row; stable, so equal
 // values keep ascending g). Rebuilt after every fold.
 void ensure_sorted(bnmc_table* t) {
-  if (t->sorted_valid) return;
+  // PST tables first: set_walk_cap / set_walk_params invalidate them without
+  // touching the sorted rows
   if (!t->pst_ready) {
     build_pst_small(t);
     t->pst_ready = true;
   }
+  if (t->sorted_valid) return;
   const uint64_t N = static_cast<uint64_t>(t->n) * t->S;
   // sorted rows padded with never-admissible entries so walk rounds need no
   // bounds checks: row stride Sw >= S + one full round
@@ -658,15 +661,31 @@ void launch_walk(bnmc_table* t, const WalkArgs& A, int C, int team_warps = 0) {
     return e && e[0] == '1';
   }();
   // speculation pays once chains settle (lower acceptance): long runs only
-  if (tw == 32 && A.perms == nullptr && !no_spec && A.iters >= 1000) {
+  if (tw == 32 && A.perms == nullptr && !no_spec && A.iters >= 1000 && !A.recheck) {
     // few chains: one 1024-thread CTA per chain evaluating kSpecD proposals per round
     walk_spec_kernel<<<C, 1024, 0, t->stream>>>(A);
     CK(cudaGetLastError());
     t->last_team = 32;
+    t->last_wu = 8;
+    t->last_spec = 1;
     return;
   }
   // deep rows (long walks): 8 entries per lane per round for small teams
   const bool deep = t->walk_deep < 0 ? t->S > kDeepRowEntries : t->walk_deep == 1;
+  if (A.recheck) {  // debug_recheck variants (results are identical for every team size)
+    const int rtw = tw >= 16 ? 32 : (tw >= 8 ? 8 : 1);
+    const int rcta = std::max(kWalkThreads, 32 * rtw);
+    const int rper = rcta / (32 * rtw);
+    const unsigned rgrid = static_cast<unsigned>((C + rper - 1) / rper);
+    if (rtw == 32) walk_chain_kernel<32, 8, true><<<rgrid, rcta, 0, t->stream>>>(A);
+    else if (rtw == 8) walk_chain_kernel<8, 8, true><<<rgrid, rcta, 0, t->stream>>>(A);
+    else walk_chain_kernel<1, kWalkUnroll, true><<<rgrid, rcta, 0, t->stream>>>(A);
+    CK(cudaGetLastError());
+    t->last_team = rtw;
+    t->last_wu = rtw >= 8 ? 8 : kWalkUnroll;
+    t->last_spec = 0;
+    return;
+  }
   switch (tw) {
     case 32: walk_chain_kernel<32><<<grid, cta, 0, t->stream>>>(A); break;
     case 16: walk_chain_kernel<16><<<grid, cta, 0, t->stream>>>(A); break;
@@ -687,6 +706,8 @@ void launch_walk(bnmc_table* t, const WalkArgs& A, int C, int team_warps = 0) {
   }
   CK(cudaGetLastError());
   t->last_team = tw;
+  t->last_wu = tw >= 8 || deep ? 8 : kWalkUnroll;
+  t->last_spec = 0;
 }
 
 WalkArgs walk_args(bnmc_table* t) {
@@ -876,6 +897,7 @@ void walk_launch(bnmc_table* t, const uint64_t* seeds, int C, const bnmc_chain_p
   A.final_order = t->d_fo.p;
   A.final_score = t->d_fs.p;
   A.accepted = t->d_acc.p;
+  A.recheck = params->debug_recheck != 0;
   cudaEvent_t e0, e1;
   CK(cudaEventCreate(&e0));
   CK(cudaEventCreate(&e1));
@@ -903,8 +925,8 @@ void walk_launch(bnmc_table* t, const uint64_t* seeds, int C, const bnmc_chain_p
   std::vector<int> amb(C, 0);
   if (!host_thr)
     CK(cudaMemcpyAsync(amb.data(), t->d_amb.p, sizeof(int) * C, cudaMemcpyDeviceToHost, t->stream));
-  unsigned long long stats[3] = {0, 0, 0};
-  CK(cudaMemcpyAsync(stats, t->stat.p, 24, cudaMemcpyDeviceToHost, t->stream));
+  unsigned long long stats[4] = {0, 0, 0, 0};
+  CK(cudaMemcpyAsync(stats, t->stat.p, 32, cudaMemcpyDeviceToHost, t->stream));
   CK(cudaStreamSynchronize(t->stream));
   float ms = 0.f;
   CK(cudaEventElapsedTime(&ms, e0, e1));
@@ -916,6 +938,7 @@ void walk_launch(bnmc_table* t, const uint64_t* seeds, int C, const bnmc_chain_p
     for (int c = 0; c < C; ++c)
       if (amb[c]) amb_out->push_back(c);
   }
+  t->last_drift_it = stats[3];
   t->last_rescans = stats[0];
   t->last_sectors = stats[1] + stats[2];  // walk path: entries visited (walked + enumerated)
   t->last_walked = stats[1];
@@ -953,8 +976,10 @@ void run_chains_walk(bnmc_table* t, const uint64_t* seeds, int C, const bnmc_cha
   std::vector<uint8_t> ta(R * it);
   std::vector<int> fo(static_cast<size_t>(R) * n), tc(R);
   std::vector<uint64_t> acc(R), tm(static_cast<size_t>(R) * K * n);
+  float replay_ms = 0.f;
   walk_launch(t, rs.data(), R, params, true, tp.data(), ta.data(), tb.data(), fo.data(), fs.data(),
-              acc.data(), tc.data(), tm.data(), tt.data(), nullptr, nullptr);
+              acc.data(), tc.data(), tm.data(), tt.data(), &replay_ms, nullptr);
+  if (device_ms) *device_ms += replay_ms;  // the replay is part of the call's device time
   for (int i = 0; i < R; ++i) {
     const size_t c = static_cast<size_t>(amb[i]);
     if (trace_proposed) std::copy_n(tp.data() + i * it, it, trace_proposed + c * it);
@@ -973,7 +998,8 @@ void run_chains_walk(bnmc_table* t, const uint64_t* seeds, int C, const bnmc_cha
   t->last_walked = keep[1];
   t->last_enumerated = keep[2];
   t->last_sectors = keep[3];
-  t->last_scan_ms = keep_ms;
+  t->last_scan_ms = keep_ms + replay_ms;
+  t->last_launches = 2;
 }
 
 int read_error(bnmc_table* t) {
@@ -1254,10 +1280,16 @@ int bnmc_gpu_run_chains(bnmc_table* t, const uint64_t* seeds, int n_chains,
       run_chains_walk(t, seeds, n_chains, params, trace_proposed, trace_accepted, trace_best,
                       final_order, final_score, accepted, tracker_count, tracker_masks,
                       tracker_totals, device_ms);
-      if (const int err = read_error(t))
+      if (const int err = read_error(t)) {
+        if (err == kErrDrift)  // RunConfig::debug_recheck, sampler.cpp:105-110
+          raise(BNMC_ERR, "chain score drifted from recomputation at iteration " +
+                              std::to_string(t->last_drift_it));
         raise(BNMC_ERR, "walk consistency check failed (" + std::to_string(err) + ")");
+      }
       return;
     }
+    if (params->debug_recheck)
+      raise(BNMC_USAGE, "debug_recheck runs on the sorted-walk path (scan_mode 0 or 2)");
     const int n = t->n, C = n_chains, K = params->track_top;
     const uint64_t iters = params->iterations;
     const ScanGeom g = scan_geometry(t, C * n);
@@ -1466,6 +1498,16 @@ int bnmc_gpu_last_walk_stats(const bnmc_table* t, uint64_t* pairs, uint64_t* wal
     if (walked) *walked = t->last_walked;
     if (enumerated) *enumerated = t->last_enumerated;
     if (sort_ms) *sort_ms = t->sort_ms;
+  });
+}
+
+int bnmc_gpu_last_walk_variant(const bnmc_table* t, int* team_warps, int* entries_per_lane,
+                               int* speculative) {
+  return guarded([&] {
+    if (!t) raise(BNMC_USAGE, "null table");
+    if (team_warps) *team_warps = t->last_team;
+    if (entries_per_lane) *entries_per_lane = t->last_wu;
+    if (speculative) *speculative = t->last_spec;
   });
 }
 

@@ -70,6 +70,8 @@ constexpr uint64_t kWalkCapDiv = 512;
 // 13.4M vs 9.0M it/s), shorter rows 4 (cfg4: 100M vs 91M it/s).
 constexpr uint64_t kDeepRowEntries = 1ull << 21;
 constexpr uint64_t kWalkBudget = BNMC_WALK_BUDGET_DEFAULT;
+constexpr int kErrDrift = 7;  // error flag: debug_recheck found a drifted chain total
+constexpr uint64_t kRecheckEvery = 100;  // sampler.cpp:105
 
 // i = base, base + stride for n <= 64 nodes and stride >= 32: at most two
 // steps, written out so the compiler does not unroll a generic strided loop.
@@ -117,7 +119,9 @@ struct WalkArgs {
   double* final_score;                 // [C]
   unsigned long long* accepted;        // [C]
   unsigned long long* stat;            // [0] pairs [1] walked entries [2] enumerated entries
+                                       // [3] first drifted iteration (debug_recheck)
   int* error;
+  int recheck;                         // RunConfig::debug_recheck
   // score-only (OrderScorer::score for C orders)
   const int* perms;                    // [C][n] or null
   uint64_t* out_masks;                 // [C][n]
@@ -595,7 +599,9 @@ __host__ __device__ constexpr int walk_cta_threads() {
 // WU: entries per lane per deep walk round (4 for rows of ~10^5-10^6 entries
 // whose walks end early; 8 for deeper rows, e.g. cfg5, where more loads in
 // flight pay).
-template <int TW, int WU = (TW >= 8 ? 8 : kWalkUnroll)>
+// RC: debug_recheck instantiation (a separate variant keeps the recheck state
+// out of the registers of the production kernel).
+template <int TW, int WU = (TW >= 8 ? 8 : kWalkUnroll), bool RC = false>
 __global__ void __launch_bounds__(walk_cta_threads<TW>(), TW == 1 ? kWalkMinBlocks1 : (TW > 8 ? 1024 / (TW * 32) : 4))
     walk_chain_kernel(WalkArgs A) {
   constexpr int kCta = walk_cta_threads<TW>();
@@ -646,11 +652,19 @@ __global__ void __launch_bounds__(walk_cta_threads<TW>(), TW == 1 ? kWalkMinBloc
   unsigned long long pairs = 0;
   double thr_t = 0.0;
   const uint64_t T = score_only ? 0 : A.iters;
-  for (uint64_t t = 0; t <= T; ++t) {
+  // rc: a debug_recheck pass (sampler.cpp:105-110) after iteration t-1: the
+  // current order is re-scored from scratch (every row, full walks, no delta
+  // or tie state) and its total compared with the chain's running total
+  uint64_t t = 0;
+  bool rc = false;
+  while (t <= T || (RC && rc)) {
+    // fresh: score every row of S.order, no proposal (recomputed at each use:
+    // a live predicate costs the production kernel a register)
+#define BNMC_FRESH (t == 0 || (RC && rc))
     // ---- proposal: propose_swap (sampler.cpp:43-52) from the split(2) stream
     if (ttid == 0) {
       int a = 0, b = n - 1;
-      if (t > 0) {
+      if (!BNMC_FRESH) {
         Rng pr{S.rng};
         a = (int)pr.next_below((uint64_t)n);
         b = (int)pr.next_below((uint64_t)(n - 1));
@@ -671,9 +685,9 @@ __global__ void __launch_bounds__(walk_cta_threads<TW>(), TW == 1 ? kWalkMinBloc
     }
     team_sync<TW>(team);
     const int pa = S.a, pb = S.b;
-    const int lo = t > 0 ? min(pa, pb) : 0, hi = t > 0 ? max(pa, pb) : n - 1;
+    const int lo = !BNMC_FRESH ? min(pa, pb) : 0, hi = !BNMC_FRESH ? max(pa, pb) : n - 1;
     for (int i = ttid; i < n; i += TW * 32) {
-      const int src = t == 0 ? i : (i == pa ? pb : (i == pb ? pa : i));
+      const int src = BNMC_FRESH ? i : (i == pa ? pb : (i == pb ? pa : i));
       S.prop[i] = S.order[src];
       S.pm[i] = S.cm[i];
       S.pb[i] = S.cb[i];
@@ -717,7 +731,7 @@ __global__ void __launch_bounds__(walk_cta_threads<TW>(), TW == 1 ? kWalkMinBloc
         // middle rows of a swap: the node at hi (X) left the predecessors, the
         // node at lo (Y) joined; eligible when the current best avoids X and
         // is not an exact tie
-        S.pd[slot] = (uint8_t)(t > 0 && p > lo && p < hi && (p <= A.pe || A.yeff) &&
+        S.pd[slot] = (uint8_t)(!BNMC_FRESH && p > lo && p < hi && (p <= A.pe || A.yeff) &&
                                !((S.tied >> v) & 1ull) && !((S.cm[v] >> S.prop[hi]) & 1ull));
         ++slot;
       }
@@ -772,10 +786,14 @@ __global__ void __launch_bounds__(walk_cta_threads<TW>(), TW == 1 ? kWalkMinBloc
       }
       if (n & 1) tot += S.pb[n - 1];
       S.total = tot;
+      if (RC && rc && tot != S.cur_total) {  // debug_recheck drift: first report wins
+        atomicCAS(A.stat + 3, 0ull, (unsigned long long)(t - 1));
+        atomicExch(A.error, kErrDrift);
+      }
       // mh_accept, sampler.cpp:54-56: log10(u) < new - old
       const double delta = tot - S.cur_total;
       bool acc = t == 0 || thr_t < delta;
-      if (t > 0 && !A.thr) {
+      if (!BNMC_FRESH && !A.thr) {
         // CUDA's log10 and glibc's may differ in the last bits: a decision
         // within the bound of the threshold is flagged, and the host replays
         // the chain with glibc thresholds (bnmc_gpu_run_chains).
@@ -785,6 +803,10 @@ __global__ void __launch_bounds__(walk_cta_threads<TW>(), TW == 1 ? kWalkMinBloc
       S.accept = acc;
     }
     team_sync<TW>(team);
+    if (RC && rc) {  // nothing of the recheck pass is committed
+      rc = false;
+      continue;
+    }
     if (score_only) {
       for (int i = ttid; i < n; i += TW * 32) {
         A.out_masks[(uint64_t)c * n + i] = S.pm[i];
@@ -826,7 +848,10 @@ __global__ void __launch_bounds__(walk_cta_threads<TW>(), TW == 1 ? kWalkMinBloc
       }
     }
     team_sync<TW>(team);
+    if constexpr (RC) rc = t > 0 && t % kRecheckEvery == 0;
+    ++t;
   }
+#undef BNMC_FRESH
   if (!score_only) {
     for (int i = ttid; i < n; i += TW * 32) A.final_order[(uint64_t)c * n + i] = S.order[i];
     if (ttid == 0) {
