@@ -485,10 +485,42 @@ McmcResult run_mcmc(const Dataset& data, const RunConfig& cfg, const PriorMatrix
                     const ScoreCache* prebuilt = nullptr);
 
 // ---- B200 extension: independent chains, chain c == run_mcmc with
-// cfg.seed = seeds[c], all run by one device launch (seed lists above 65,536
-// are processed in groups of that size).
-std::vector<McmcResult> run_chains(const ScoreCache& cache, const PriorMatrix& priors,
-                                   const RunConfig& cfg, std::span<const std::uint64_t> seeds);
+// cfg.seed = seeds[c], all run by one device launch. The device writes every
+// chain's trace, tracker and final state straight into page-locked host
+// buffers (pooled and reused across calls); a chain's McmcResult is built only
+// when it is accessed.
+class ChainResults {
+ public:
+  std::size_t size() const { return seeds_.size(); }
+  std::uint64_t iterations() const { return iters_; }
+  std::uint64_t seed(std::size_t c) const { return seeds_.at(c); }
+  McmcResult operator[](std::size_t c) const;  // built on access
+  std::vector<McmcResult> to_vector() const;
+  // raw per-chain views (valid while this object lives)
+  std::span<const double> trace_proposed(std::size_t c) const;
+  std::span<const std::uint8_t> trace_accepted(std::size_t c) const;
+  std::span<const double> trace_best(std::size_t c) const;
+  std::span<const int> final_order(std::size_t c) const;
+  double final_score(std::size_t c) const;
+  std::uint64_t accepted(std::size_t c) const;
+  double best_score(std::size_t c) const;  // tracker best
+  double device_ms() const { return device_ms_; }  // device time of the chain kernel(s)
+  double sampling_seconds() const { return wall_; }  // wall time of the device call
+
+  struct Buffers;  // page-locked blocks (dropin.cpp)
+
+ private:
+  friend ChainResults run_chains(const class ScoreCache&, const PriorMatrix&, const RunConfig&,
+                                 std::span<const std::uint64_t>);
+  std::shared_ptr<Buffers> buf_;
+  std::vector<std::uint64_t> seeds_;
+  std::uint64_t iters_ = 0;
+  int n_ = 0, K_ = 0;
+  double device_ms_ = 0.0, wall_ = 0.0;
+};
+
+ChainResults run_chains(const ScoreCache& cache, const PriorMatrix& priors, const RunConfig& cfg,
+                        std::span<const std::uint64_t> seeds);
 
 }  // namespace bnmc
 

@@ -77,6 +77,12 @@ int bnmc_gpu_version(void);
 /* Number of usable sm_100 devices (0 when none; status 5 when the runtime fails). */
 int bnmc_gpu_device_count(int* out);
 
+/* Page-locked (pinned) host memory for result buffers: device->host copies of
+ * run_chains outputs into it run at full PCIe/C2C bandwidth and need no
+ * staging. bytes == 0 yields NULL. Free with bnmc_gpu_host_free. */
+int bnmc_gpu_host_alloc(uint64_t bytes, void** out);
+int bnmc_gpu_host_free(void* p);
+
 /* S(n-1,s) * 8: ScoreCache::estimate_bytes (scoring.cpp:157-160). */
 uint64_t bnmc_gpu_table_estimate_bytes(int n, int s);
 /* S(c,s) = sum_{j<=s} C(c,j): bounded_subset_count (combinatorics.hpp:32-36). */

@@ -40,6 +40,8 @@ SIGNATURES = {
     "bnmc_gpu_last_error_message": (C.c_char_p, []),
     "bnmc_gpu_version": (C.c_int, []),
     "bnmc_gpu_device_count": (C.c_int, [C.POINTER(C.c_int)]),
+    "bnmc_gpu_host_alloc": (C.c_int, [C.c_uint64, C.POINTER(_vp)]),
+    "bnmc_gpu_host_free": (C.c_int, [_vp]),
     "bnmc_gpu_table_estimate_bytes": (C.c_uint64, [C.c_int, C.c_int]),
     "bnmc_gpu_bounded_subset_count": (C.c_uint64, [C.c_int, C.c_int]),
     "bnmc_gpu_table_build": (C.c_int, [_u8p, _i32p, C.c_uint64, C.c_int, C.POINTER(ScoreParams),
@@ -147,3 +149,41 @@ def device_count() -> int:
     n = C.c_int()
     check(lib().bnmc_gpu_device_count(C.byref(n)))
     return n.value
+
+
+# ---- pinned host buffers (bnmc_gpu_host_alloc) with a small reuse pool: a
+# block returns to the pool when the last numpy view of it is collected, so
+# repeated run_chains calls reuse page-locked memory without staging copies.
+_POOL: dict = {}
+_POOL_BYTES = [0]
+_POOL_CAP = 8 << 30
+
+
+def _release(ptr: int, nbytes: int):
+    try:
+        if _POOL_BYTES[0] + nbytes <= _POOL_CAP:
+            _POOL.setdefault(nbytes, []).append(ptr)
+            _POOL_BYTES[0] += nbytes
+        elif _lib is not None:
+            _lib.bnmc_gpu_host_free(ptr)
+    except Exception:  # interpreter shutdown
+        pass
+
+
+def pinned_empty(shape, dtype) -> np.ndarray:
+    """np.empty(shape, dtype) in page-locked host memory owned by the library."""
+    import weakref
+    dtype = np.dtype(dtype)
+    count = int(np.prod(shape)) if len(shape) else 1
+    nbytes = max(8, count * dtype.itemsize)
+    free = _POOL.get(nbytes)
+    if free:
+        ptr = free.pop()
+        _POOL_BYTES[0] -= nbytes
+    else:
+        out = _vp()
+        check(lib().bnmc_gpu_host_alloc(nbytes, C.byref(out)))
+        ptr = out.value
+    buf = (C.c_char * nbytes).from_address(ptr)
+    weakref.finalize(buf, _release, ptr, nbytes)
+    return np.frombuffer(buf, dtype=dtype, count=count).reshape(shape)

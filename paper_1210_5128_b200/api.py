@@ -14,6 +14,7 @@ from __future__ import annotations
 
 import ctypes as C
 import enum
+from collections.abc import Sequence
 import struct
 import time
 from dataclasses import dataclass, field
@@ -502,10 +503,51 @@ class ChainBatch:
     device_ms: float
     wall_s: float
 
+    @classmethod
+    def allocate(cls, chains: int, iterations: int, n: int, track_top: int, pinned: bool = True):
+        """Result buffers for `chains` chains; page-locked (bnmc_gpu_host_alloc,
+        pooled) unless pinned=False."""
+        E = _lib.pinned_empty if pinned else (lambda shape, dt: np.empty(shape, dt))
+        c, i, K = chains, iterations, track_top
+        return cls(E((c, i), np.float64), E((c, i), np.uint8), E((c, i), np.float64),
+                   E((c, n), np.int32), E((c,), np.float64), E((c,), np.uint64),
+                   E((c,), np.int32), E((c, K, n), np.uint64), E((c, K), np.float64), 0.0, 0.0)
+
+    def result(self, c: int, seed: int = 0) -> McmcResult:
+        """McmcResult of chain c as views into the batch buffers (no copies)."""
+        k = int(self.tracker_count[c])
+        return McmcResult(
+            tracker_masks=self.tracker_masks[c, :k], tracker_totals=self.tracker_totals[c, :k],
+            trace_proposed=self.trace_proposed[c], trace_accepted=self.trace_accepted[c].view(np.bool_),
+            trace_best=self.trace_best[c], final_order=self.final_order[c],
+            final_score=float(self.final_score[c]), accepted=int(self.accepted[c]),
+            sampling_seconds=self.wall_s, device_ms=self.device_ms, seed=seed)
+
+
+class ChainResults(Sequence):
+    """run_chains' result: a sequence of McmcResult built on access from one
+    ChainBatch in pinned host memory (no per-chain staging or copies)."""
+
+    def __init__(self, batch: ChainBatch, seeds):
+        self.batch = batch
+        self.seeds = np.asarray(seeds, np.uint64)
+
+    def __len__(self):
+        return int(self.seeds.size)
+
+    def __getitem__(self, i):
+        if isinstance(i, slice):
+            return [self[j] for j in range(*i.indices(len(self)))]
+        if i < 0:
+            i += len(self)
+        if not 0 <= i < len(self):
+            raise IndexError(i)
+        return self.batch.result(i, int(self.seeds[i]))
+
 
 def run_chains_batch(cache: ScoreCache, priors, seeds, cfg: RunConfig, out: ChainBatch | None = None):
     """Independent chains through one bnmc_gpu_run_chains call; chain c is run_mcmc
-    with seed seeds[c]. Host buffers may be passed in `out` (reused, e.g. pinned)."""
+    with seed seeds[c]. Results land in `out` (reused) or in fresh pinned buffers."""
     cfg.validate()
     pr = _prior_array(priors)
     if pr is not None and pr.shape[0] != cache.n():
@@ -514,10 +556,7 @@ def run_chains_batch(cache: ScoreCache, priors, seeds, cfg: RunConfig, out: Chai
     nc, n, K, it = seeds.size, cache.n(), cfg.track_top, cfg.iterations
     cache.bind_priors(pr)
     if out is None:
-        out = ChainBatch(np.empty((nc, it)), np.empty((nc, it), np.uint8), np.empty((nc, it)),
-                         np.empty((nc, n), np.int32), np.empty(nc), np.empty(nc, np.uint64),
-                         np.empty(nc, np.int32), np.empty((nc, K, n), np.uint64),
-                         np.empty((nc, K)), 0.0, 0.0)
+        out = ChainBatch.allocate(nc, it, n, K)
     ms = C.c_float()
     params = _lib.ChainParams(it, K, int(cfg.strict_paper_tracker), cfg.scan_mode, 0,
                               cfg.team_warps, cfg.exact_accept, cfg.accept_tol_log2,
@@ -533,19 +572,11 @@ def run_chains_batch(cache: ScoreCache, priors, seeds, cfg: RunConfig, out: Chai
     return out
 
 
-def run_chains(cache: ScoreCache, priors, seeds, cfg: RunConfig):
-    """Independent chains (chain c == run_mcmc with seed seeds[c]) in one device loop."""
-    b = run_chains_batch(cache, priors, seeds, cfg)
-    res = []
-    for c in range(b.final_score.size):
-        k = int(b.tracker_count[c])
-        res.append(McmcResult(
-            tracker_masks=b.tracker_masks[c, :k].copy(), tracker_totals=b.tracker_totals[c, :k].copy(),
-            trace_proposed=b.trace_proposed[c].copy(), trace_accepted=b.trace_accepted[c].astype(bool),
-            trace_best=b.trace_best[c].copy(), final_order=b.final_order[c].copy(),
-            final_score=float(b.final_score[c]), accepted=int(b.accepted[c]),
-            sampling_seconds=b.wall_s, device_ms=b.device_ms, seed=int(seeds[c])))
-    return res
+def run_chains(cache: ScoreCache, priors, seeds, cfg: RunConfig, out: ChainBatch | None = None):
+    """Independent chains (chain c == run_mcmc with seed seeds[c]) in one device
+    loop -> ChainResults (McmcResult per chain, built lazily over pinned buffers)."""
+    seeds = np.ascontiguousarray(seeds, dtype=np.uint64)
+    return ChainResults(run_chains_batch(cache, priors, seeds, cfg, out), seeds)
 
 
 def run_mcmc(data: Dataset, cfg: RunConfig, priors=None, prebuilt: ScoreCache | None = None):

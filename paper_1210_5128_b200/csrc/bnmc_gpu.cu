@@ -1036,6 +1036,23 @@ int bnmc_gpu_device_count(int* out) {
   });
 }
 
+int bnmc_gpu_host_alloc(uint64_t bytes, void** out) {
+  return guarded([&] {
+    if (!out) raise(BNMC_USAGE, "null output pointer");
+    *out = nullptr;
+    int count = 0;
+    CK(cudaGetDeviceCount(&count));
+    if (bytes == 0) return;
+    CK(cudaHostAlloc(out, bytes, cudaHostAllocPortable));
+  });
+}
+
+int bnmc_gpu_host_free(void* p) {
+  return guarded([&] {
+    if (p) CK(cudaFreeHost(p));
+  });
+}
+
 uint64_t bnmc_gpu_table_estimate_bytes(int n, int s) {
   return static_cast<uint64_t>(n) * bounded_count(n - 1, s) * 8;
 }

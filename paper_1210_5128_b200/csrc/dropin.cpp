@@ -12,6 +12,8 @@
 #include <chrono>
 #include <cstring>
 #include <fstream>
+#include <map>
+#include <memory>
 #include <mutex>
 #include <numeric>
 
@@ -639,57 +641,148 @@ bool mh_accept(double old_score, double new_score, Rng& rng) {  // sampler.cpp:5
   return std::log10(rng.next_unit_open()) < new_score - old_score;
 }
 
-std::vector<McmcResult> run_chains(const ScoreCache& cache, const PriorMatrix& priors,
-                                   const RunConfig& cfg, std::span<const std::uint64_t> seeds) {
-  cfg.validate();
-  if (priors.n() != cache.n()) throw DataError("prior matrix does not match the dataset's node count");
-  cache.bind_priors(priors);
-  const int n = cache.n(), K = cfg.track_top;
-  const std::uint64_t iters = cfg.iterations;
-  std::vector<McmcResult> out;
-  out.reserve(seeds.size());
-  // one device call for any number of chains (the sorted-walk path has no
-  // per-call chain limit); groups only bound the host staging buffers
-  constexpr std::size_t kGroup = std::size_t{1} << 16;
-  for (std::size_t c0 = 0; c0 < seeds.size(); c0 += kGroup) {
-    const int C = static_cast<int>(std::min(kGroup, seeds.size() - c0));
-    std::vector<double> tp(C * iters), tb(C * iters), fs(C), tt(static_cast<std::size_t>(C) * K);
-    std::vector<std::uint8_t> ta(C * iters);
-    std::vector<int> fo(static_cast<std::size_t>(C) * n), tc(C);
-    std::vector<std::uint64_t> acc(C), tm(static_cast<std::size_t>(C) * K * n);
-    bnmc_chain_params params{};
-    params.iterations = iters;
-    params.track_top = K;
-    params.strict = cfg.strict_paper_tracker ? 1 : 0;
-    params.debug_recheck = cfg.debug_recheck ? 1 : 0;  // device rescore every 100 iterations
-    const auto t0 = std::chrono::steady_clock::now();
-    check(bnmc_gpu_run_chains(cache.device_table(), seeds.data() + c0, C, &params, tp.data(),
-                              ta.data(), tb.data(), fo.data(), fs.data(), acc.data(), tc.data(),
-                              tm.data(), tt.data(), nullptr));
-    const double wall = seconds_since(t0);
-    for (int c = 0; c < C; ++c) {
-      McmcResult r{BestGraphTracker(K), {}, Order(), 0.0, 0, 0.0, 0.0};
-      // Device tracker entries are already in tracker order; re-offering them
-      // in that order rebuilds the identical vector.
-      for (int e = 0; e < tc[c]; ++e) {
-        std::vector<ParentSet> ps(n);
-        for (int v = 0; v < n; ++v)
-          ps[v] = ParentSet{tm[(static_cast<std::size_t>(c) * K + e) * n + v]};
-        r.tracker.update({Dag(std::move(ps)), tt[static_cast<std::size_t>(c) * K + e]});
-      }
-      r.trace.reserve(iters);
-      for (std::uint64_t t = 0; t < iters; ++t) {
-        const std::size_t o = static_cast<std::size_t>(c) * iters + t;
-        r.trace.push_back({t + 1, tp[o], ta[o] != 0, tb[o]});
-      }
-      r.final_order = Order(std::vector<int>(fo.begin() + static_cast<long>(c) * n,
-                                             fo.begin() + static_cast<long>(c + 1) * n));
-      r.final_score = fs[c];
-      r.accepted = acc[c];
-      r.sampling_seconds = wall;
-      out.push_back(std::move(r));
+// ---- run_chains: results in pooled page-locked host memory, McmcResult on access
+namespace {
+std::mutex g_pool_mu;
+std::map<std::size_t, std::vector<void*>> g_pool;  // bytes -> free pinned blocks
+std::size_t g_pool_bytes = 0;
+constexpr std::size_t kPoolCap = std::size_t{8} << 30;
+
+void* pinned_take(std::size_t bytes) {
+  {
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    auto it = g_pool.find(bytes);
+    if (it != g_pool.end() && !it->second.empty()) {
+      void* p = it->second.back();
+      it->second.pop_back();
+      g_pool_bytes -= bytes;
+      return p;
     }
   }
+  void* p = nullptr;
+  check(bnmc_gpu_host_alloc(bytes, &p));
+  return p;
+}
+
+void pinned_give(void* p, std::size_t bytes) {
+  if (!p) return;
+  {
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    if (g_pool_bytes + bytes <= kPoolCap) {
+      g_pool[bytes].push_back(p);
+      g_pool_bytes += bytes;
+      return;
+    }
+  }
+  bnmc_gpu_host_free(p);
+}
+}  // namespace
+
+struct ChainResults::Buffers {
+  struct Block {
+    void* p = nullptr;
+    std::size_t bytes = 0;
+  };
+  Block tp, ta, tb, fo, fs, acc, tc, tm, tt;
+  template <class T>
+  T* take(Block& b, std::size_t count) {
+    b.bytes = std::max<std::size_t>(8, count * sizeof(T));
+    b.p = pinned_take(b.bytes);
+    return static_cast<T*>(b.p);
+  }
+  ~Buffers() {
+    for (Block* b : {&tp, &ta, &tb, &fo, &fs, &acc, &tc, &tm, &tt}) pinned_give(b->p, b->bytes);
+  }
+};
+
+std::span<const double> ChainResults::trace_proposed(std::size_t c) const {
+  return {static_cast<const double*>(buf_->tp.p) + c * iters_, iters_};
+}
+std::span<const std::uint8_t> ChainResults::trace_accepted(std::size_t c) const {
+  return {static_cast<const std::uint8_t*>(buf_->ta.p) + c * iters_, iters_};
+}
+std::span<const double> ChainResults::trace_best(std::size_t c) const {
+  return {static_cast<const double*>(buf_->tb.p) + c * iters_, iters_};
+}
+std::span<const int> ChainResults::final_order(std::size_t c) const {
+  return {static_cast<const int*>(buf_->fo.p) + c * n_, static_cast<std::size_t>(n_)};
+}
+double ChainResults::final_score(std::size_t c) const { return static_cast<const double*>(buf_->fs.p)[c]; }
+std::uint64_t ChainResults::accepted(std::size_t c) const {
+  return static_cast<const std::uint64_t*>(buf_->acc.p)[c];
+}
+double ChainResults::best_score(std::size_t c) const {
+  return static_cast<const double*>(buf_->tt.p)[c * K_];
+}
+
+McmcResult ChainResults::operator[](std::size_t c) const {
+  if (c >= size()) throw UsageError("chain index out of range");
+  McmcResult r{BestGraphTracker(K_), {}, Order(), 0.0, 0, 0.0, 0.0};
+  const int count = static_cast<const int*>(buf_->tc.p)[c];
+  const auto* tm = static_cast<const std::uint64_t*>(buf_->tm.p);
+  const auto* tt = static_cast<const double*>(buf_->tt.p);
+  // Device tracker entries are already in tracker order; re-offering them in
+  // that order rebuilds the identical vector.
+  for (int e = 0; e < count; ++e) {
+    std::vector<ParentSet> ps(n_);
+    for (int v = 0; v < n_; ++v) ps[v] = ParentSet{tm[(c * K_ + e) * n_ + v]};
+    r.tracker.update({Dag(std::move(ps)), tt[c * K_ + e]});
+  }
+  const auto tp = trace_proposed(c);
+  const auto ta = trace_accepted(c);
+  const auto tb = trace_best(c);
+  r.trace.resize(iters_);
+  for (std::uint64_t t = 0; t < iters_; ++t) r.trace[t] = {t + 1, tp[t], ta[t] != 0, tb[t]};
+  const auto fo = final_order(c);
+  r.final_order = Order(std::vector<int>(fo.begin(), fo.end()));
+  r.final_score = final_score(c);
+  r.accepted = accepted(c);
+  r.sampling_seconds = wall_;
+  return r;
+}
+
+std::vector<McmcResult> ChainResults::to_vector() const {
+  std::vector<McmcResult> out(size(), McmcResult{BestGraphTracker(std::max(K_, 1)), {}, Order(), 0.0, 0, 0.0, 0.0});
+#pragma omp parallel for schedule(dynamic, 64)
+  for (std::size_t c = 0; c < size(); ++c) out[c] = (*this)[c];
+  return out;
+}
+
+ChainResults run_chains(const ScoreCache& cache, const PriorMatrix& priors, const RunConfig& cfg,
+                        std::span<const std::uint64_t> seeds) {
+  cfg.validate();
+  if (priors.n() != cache.n()) throw DataError("prior matrix does not match the dataset's node count");
+  if (seeds.empty()) throw UsageError("run_chains needs at least one seed");
+  if (seeds.size() > 0x7fffffffu) throw UsageError("too many chains for one call");
+  cache.bind_priors(priors);
+  ChainResults out;
+  out.seeds_.assign(seeds.begin(), seeds.end());
+  out.iters_ = cfg.iterations;
+  out.n_ = cache.n();
+  out.K_ = cfg.track_top;
+  const std::size_t C = seeds.size(), I = cfg.iterations, n = cache.n(), K = cfg.track_top;
+  auto b = std::make_shared<ChainResults::Buffers>();
+  double* tp = b->take<double>(b->tp, C * I);
+  std::uint8_t* ta = b->take<std::uint8_t>(b->ta, C * I);
+  double* tb = b->take<double>(b->tb, C * I);
+  int* fo = b->take<int>(b->fo, C * n);
+  double* fs = b->take<double>(b->fs, C);
+  std::uint64_t* acc = b->take<std::uint64_t>(b->acc, C);
+  int* tc = b->take<int>(b->tc, C);
+  std::uint64_t* tm = b->take<std::uint64_t>(b->tm, C * K * n);
+  double* tt = b->take<double>(b->tt, C * K);
+  bnmc_chain_params params{};
+  params.iterations = cfg.iterations;
+  params.track_top = cfg.track_top;
+  params.strict = cfg.strict_paper_tracker ? 1 : 0;
+  params.debug_recheck = cfg.debug_recheck ? 1 : 0;  // device rescore every 100 iterations
+  float ms = 0.f;
+  const auto t0 = std::chrono::steady_clock::now();
+  check(bnmc_gpu_run_chains(cache.device_table(), seeds.data(), static_cast<int>(C), &params, tp,
+                            ta, tb, fo, fs, acc, tc, tm, tt, &ms));
+  out.wall_ = seconds_since(t0);
+  out.device_ms_ = ms;
+  out.buf_ = std::move(b);
   return out;
 }
 
@@ -706,7 +799,7 @@ McmcResult run_mcmc(const Dataset& data, const RunConfig& cfg, const PriorMatrix
   const ScoreCache& active = prebuilt ? *prebuilt : built;
   const double pre = seconds_since(t_pre);
   const std::uint64_t seed = cfg.seed;
-  McmcResult r = std::move(run_chains(active, priors, cfg, std::span<const std::uint64_t>(&seed, 1)).front());
+  McmcResult r = run_chains(active, priors, cfg, std::span<const std::uint64_t>(&seed, 1))[0];
   r.preprocess_seconds = pre;
   return r;
 }

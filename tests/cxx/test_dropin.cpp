@@ -521,8 +521,13 @@ TEST_CASE("run_chains: chain c equals run_mcmc with seed c", true) {
   const PriorMatrix neutral = PriorMatrix::neutral(12);
   std::vector<std::uint64_t> seeds(70);
   std::iota(seeds.begin(), seeds.end(), 1);
-  const std::vector<McmcResult> all = run_chains(cache, neutral, cfg, seeds);
+  const ChainResults all = run_chains(cache, neutral, cfg, seeds);
   REQUIRE(all.size() == seeds.size());
+  const std::vector<McmcResult> vec = all.to_vector();
+  REQUIRE(vec.size() == seeds.size());
+  CHECK(vec[41].final_score == all.final_score(41));
+  CHECK(vec[41].trace.size() == cfg.iterations);
+  CHECK(all.trace_proposed(41)[7] == vec[41].trace[7].proposed_score);
   for (std::size_t c : {std::size_t{0}, std::size_t{41}, std::size_t{69}}) {
     RunConfig one = cfg;
     one.seed = seeds[c];
