@@ -102,15 +102,55 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
-def ncu_traffic(kernel):
-    """DRAM bytes per launch of `kernel` from the committed ncu capture
-    (profiles/ncu_traffic.json, written from an ncu --set full report of this
-    bench's configuration), or None."""
+def ncu_profile(kernel):
+    """ncu --set full figures of `kernel` at this bench's configuration
+    (profiles/ncu_traffic.json, written by tools/ncu_traffic.py from the
+    round's capture): DRAM bytes, warp instructions, IPC, issue-slot use per
+    launch and the capture it came from; {} when absent."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            return float(json.load(f)[kernel]["dram_bytes_per_launch"])
+            return dict(json.load(f)[kernel])
     except Exception:
+        return {}
+
+
+class _HostData:
+    """Dataset-shaped view of host arrays (n, rows(), cells, cards)."""
+
+    def __init__(self, cells, cards):
+        self.cells, self.cards, self.n = cells, np.asarray(cards, np.int32), int(cells.shape[1])
+
+    def rows(self):
+        return int(self.cells.shape[0])
+
+
+def reference_precompute(data, s, samples=4000, seed=0):
+    """The reference's ScoreCache::build time at this config on this host,
+    extrapolated from local_score (count_statistics + local_score_from_counts,
+    scoring.cpp:82-141, the per-entry body of the build loop at
+    scoring.cpp:179-190) on uniformly sampled table entries, single-threaded,
+    x entries / OpenMP threads (linear scaling: optimistic for the reference).
+    SURVEY §8(d) prescribes this when the full build does not fit the run."""
+    from oracle import ref
+    if not ref.available():
         return None
+    n, m = data.n, data.rows()
+    S = ref.bounded_subset_count(n - 1, s)
+    rng = np.random.default_rng(seed)
+    ents = []
+    for _ in range(samples):
+        v = int(rng.integers(n))
+        cm = ref.subset_at(int(rng.integers(S)), n - 1, s)
+        low = cm & ((1 << v) - 1)
+        ents.append((v, low | ((cm >> v) << (v + 1))))
+    _, sec = ref.local_score_batch(data.cells, data.cards, [v for v, _ in ents],
+                                   [pm for _, pm in ents])
+    per = sec / samples
+    threads = ref.max_threads()
+    return {"precompute_s": per * n * S / threads, "seconds_per_entry_1thread": per,
+            "entries": n * S, "threads": threads, "sampled_entries": samples,
+            "method": "reference local_score on uniformly sampled entries, single thread, "
+                      "x n*S(n-1,s) / OpenMP threads (SURVEY 8(d))"}
 
 
 def flush_l2(torch, buf):
@@ -193,6 +233,35 @@ def cpu_baseline(rc, n, s, priors, ours_trace, iters, seed):
             "trace_bit_exact_vs_gpu": parity}
 
 
+def walk_roofline(prof, avg_launch_s, peak, peak_src, alg_bytes, chain_iters_per_launch):
+    """Roofline of the fused walk kernel (K2W). Its working set (the touched
+    tops of the sorted rows) is L2-resident: DRAM moves ~9 GB per launch while
+    the walk touches ~450 GB of sorted entries, so HBM is not its bound; it is
+    bound by instruction issue and L2 latency. `achieved`/`frac` are the MEASURED
+    DRAM bytes per launch (ncu capture of this configuration) over this run's
+    launch time against the HBM peak; `issue` carries the ncu instruction
+    count, IPC and issue-slot use that do bound it."""
+    dram = prof.get("dram_bytes_per_launch")
+    ach = dram / avg_launch_s / 1e9 if dram else None
+    inst = prof.get("warp_instructions")
+    return {"bound": "issue/L2 (latency)", "achieved": ach, "peak": peak, "unit": "GB/s",
+            "frac": ach / peak if ach else None, "traffic": dram,
+            "traffic_source": prof.get("source"),
+            "kernel": "walk_chain_kernel (K2W: fused scan + chain step)",
+            "peak_source": peak_src, "avg_launch_us": avg_launch_s * 1e6,
+            "issue": {"warp_instructions_per_launch": inst,
+                      "warp_instructions_per_chain_iteration":
+                          inst / chain_iters_per_launch if inst else None,
+                      "ipc": prof.get("ipc"), "ipc_peak": 4.0,
+                      "issue_slots_busy": prof.get("issue_slots_busy"),
+                      "top_stalls": prof.get("top_stalls")},
+            "walked_bytes_per_launch": alg_bytes,
+            "walked_GBps": alg_bytes / avg_launch_s / 1e9,
+            "note": "walked bytes = sorted entries walked x 16 B + enumerated local scores x 8 B "
+                    "(counted on the device); they are served by L1/L2, DRAM traffic is the "
+                    "ncu-measured figure"}
+
+
 def full_scan_probe(P, _lib, cache, pri, cfg, chains=64, iters=100):
     """The full-row scan path (scan_mode 1, K2 + CUDA Graphs): it/s and the K2
     roofline (32-B key sectors it must stream per launch / avg launch time)."""
@@ -225,19 +294,21 @@ def run_ours(args):
 
     rank, world, local = D.env_rank_world()
     torch.cuda.set_device(local)
-    group = None
-    # --force-dist exercises the multi-GPU code path (NCCL process group, row
-    # all-gather, record gather, max-over-ranks) even at world size 1
+    # --force-dist exercises the multi-GPU code path (the library's NCCL
+    # communicator: split K1 + all-reduce, record all-gather, max over ranks)
+    # even at world size 1; torch.distributed (gloo) only ships the NCCL id
     dist_on = world > 1 or args.force_dist
+    comm = None
     if dist_on:
         import torch.distributed as tdist
-        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        tdist.init_process_group("gloo")
+        comm = D.Comm(rank, world, local)
     data, pri, cfg, truth = P.baseline_instance(args.config)
     cfg.device = local
-    # ---- precompute: row-sharded K1 + NCCL all-gather, then the per-row sort
+    # ---- precompute: K1 split over the ranks + NCCL all-reduce, then the per-row sort
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    cache = D.build_table_sharded(data, cfg, pri, rank, world, group, force=dist_on)
+    cache = D.build_table_comm(data, cfg, pri, comm) if dist_on else P.ScoreCache.build(data, cfg, pri)
     cfg.iterations, cfg.scan_mode = 1, 2
     P.run_chains_batch(cache, pri, [1], cfg)  # binds priors, builds the sorted rows
     torch.cuda.synchronize()
@@ -262,6 +333,7 @@ def run_ours(args):
     if dist_on:
         import torch.distributed as tdist
         tdist.barrier()
+        comm.max([0.0])  # NCCL rendezvous before the timed region
     torch.cuda.synchronize()
     dev_ms, wall_s, walked, enumerated, pairs, replayed = [], [], 0, 0, 0, 0
     with ClockSampler(local) as clocks:
@@ -284,12 +356,10 @@ def run_ours(args):
     tot_dev = sum(dev_ms) / 1e3
     tot_wall = sum(wall_s)
     recs = D.chain_records_from_batch(out, D.chain_seeds(1, rank, Cn, args.steps - 1, world), n)
-    if dist_on:
-        import torch.distributed as tdist
-        tt = torch.tensor([tot_dev, tot_wall, pre_s], device="cuda", dtype=torch.float64)
-        tdist.all_reduce(tt, op=tdist.ReduceOp.MAX)
-        tot_dev, tot_wall, pre_s = tt.tolist()
-        allrec = D.gather_chain_records(recs, group, device="cuda")
+    k1_ms = k1.value
+    if dist_on:  # max over ranks; records all-gathered over the library's NCCL comm
+        tot_dev, tot_wall, pre_s, k1_ms = comm.max([tot_dev, tot_wall, pre_s, k1_ms])
+        allrec = comm.allgather(recs).reshape(-1, recs.shape[1])
     else:
         allrec = recs
     iters_total = args.steps * Cn * I * world
@@ -318,6 +388,10 @@ def run_ours(args):
                              memory_cap_bytes=cfg.memory_cap_bytes, device=local, scan_mode=2)
             ours1 = P.run_chains(cache, pri, [1], c1)[0]
             cpu = cpu_baseline(rc, n, cfg.max_parents, pri, ours1.trace_proposed, args.cpu_iters, 1)
+            rp = reference_precompute(data, cfg.max_parents)
+            if cpu is not None and rp is not None:
+                cpu["precompute_s"] = rp["precompute_s"]
+                cpu["precompute"] = rp
         if world == 1 and not args.no_extras:
             # one chain (the reference's own unit of work): latency-bound, the
             # speculative single-chain kernel runs at >= 1000 iterations
@@ -347,21 +421,13 @@ def run_ours(args):
                     "d2h_bytes_per_step": d2h,
                     "note": "bnmc_gpu_run_chains with host seeds in, pinned host trace/tracker/"
                             "final-state buffers out; wall time per call"},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": ncu_traffic("walk_chain_kernel"),
-                         "kernel": "walk_chain_kernel (K2W: fused scan + chain step)",
-                         "peak_source": peak_src, "bytes_per_launch": bytes_per_launch,
-                         "avg_launch_us": avg_launch_s * 1e6,
-                         "note": "algorithmic bytes = sorted entries walked x 16 B + PST-enumerated "
-                                 "local scores x 8 B; the touched tops of the sorted rows are "
-                                 "L2-resident (traffic = ncu DRAM bytes per launch, well below the "
-                                 "algorithmic bytes), so the kernel is latency/issue-bound, not "
-                                 "HBM-bound"},
+            "roofline": walk_roofline(ncu_profile("walk_chain_kernel"), avg_launch_s, peak,
+                                      peak_src, bytes_per_launch, args.steps * Cn * I / args.steps),
             "walk": {"pairs_per_iteration": pairs / (args.steps * Cn * (I + 1)),
                      "walked_per_pair": walked / max(1, pairs),
                      "enumerated_per_pair": enumerated / max(1, pairs),
                      "chains_replayed_exact": replayed},
-            "precompute_s": pre_s, "precompute_kernel_ms": k1.value, "fold_ms": fold.value,
+            "precompute_s": pre_s, "precompute_kernel_ms": k1_ms, "fold_ms": fold.value,
             "gpu_launches": int(args.steps * (1 + (1 if replayed else 0))),
             "best_total": best["best_total"], "best_chain_seed": best["seed"],
             "cpu_baseline": cpu,
@@ -372,6 +438,7 @@ def run_ours(args):
     if dist_on:
         import torch.distributed as tdist
         tdist.barrier()
+        comm.close()
         tdist.destroy_process_group()
     return out_line
 
@@ -404,6 +471,8 @@ def run_reference(args):
         r = ref.run_mcmc(cells, cards, k, I, 1 + step, priors=pri, prebuilt=cache)
         samp += r.sampling_seconds
     value = args.steps * I / samp
+
+    rp = reference_precompute(_HostData(cells, cards), k)
     sample = (f"{args.steps} x {I} run_mcmc iterations (OrderScorer::score, OpenMP "
               f"{ref.max_threads()} threads) on a cache built by ScoreCache::build from the first "
               f"{m_build} of {m} rows ({build_s:.1f}s; the order scan is independent of m)")
@@ -416,7 +485,9 @@ def run_reference(args):
                                   f"1 chain x {I} iterations per step"},
            "cpu_baseline": {"value": value, "unit": "iterations/s", "cores": ref.max_threads(),
                             "cpu_model": cpu_model(),
-                            "kind": "reference", "sample": sample},
+                            "kind": "reference", "sample": sample,
+                            "precompute_s": rp["precompute_s"] if rp else None,
+                            "precompute": rp},
            "e2e": {"value": value, "unit": "iterations/s", "h2d_bytes_per_step": 0,
                    "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)

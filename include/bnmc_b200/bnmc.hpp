@@ -43,6 +43,7 @@
 #include <stdexcept>
 #include <string>
 #include <utility>
+#include <map>
 #include <vector>
 
 #include "../bnmc_gpu.h"
@@ -179,6 +180,8 @@ struct RunConfig {
   std::uint64_t memory_cap_bytes = std::uint64_t{4} << 30;
   bool debug_recheck = false;
   int device = 0;  // extension: CUDA ordinal of the table
+  int n_gpus = 1;  // extension: > 1 = devices device..device+n_gpus-1 (split precompute
+                   // + NCCL all-reduce, chains spread over full replicas)
 
   void validate() const;
 };
@@ -283,28 +286,38 @@ struct Hyperparams {
   friend bool operator==(const Hyperparams&, const Hyperparams&) = default;
 };
 
-// N_ijk for one (node, parent set), counted on the device
-// (bnmc_gpu_count_statistics). Dense: configs() x child_card() u32 cells,
-// config index mixed-radix with the lowest parent least significant.
+// N_ijk for one (node, parent set), counted on the device. Like the
+// reference's CountTable (scoring.hpp:41-77, scoring.cpp:53-80): dense
+// configs() x child_card() u32 cells up to 2^22 cells
+// (bnmc_gpu_count_statistics), otherwise an ordered map of the active
+// configurations (bnmc_gpu_count_statistics_sparse); the config index is
+// mixed-radix with the lowest parent least significant; iteration ascending.
 class CountTable {
  public:
   CountTable(std::uint64_t configs, int child_card);
   std::uint64_t configs() const { return r_; }
   int child_card() const { return card_; }
   std::uint64_t samples() const;
-  std::uint32_t njk(std::uint64_t config, int state) const { return cells_[config * card_ + state]; }
+  std::uint32_t njk(std::uint64_t config, int state) const;
   std::uint32_t nk(std::uint64_t config) const;
   template <class F>
   void for_each_active(F&& f) const {  // configs with N_ik > 0, ascending
-    for (std::uint64_t k = 0; k < r_; ++k)
-      if (nk(k) > 0) f(k, cells_.data() + k * card_);
+    if (dense()) {
+      for (std::uint64_t k = 0; k < r_; ++k)
+        if (nk(k) > 0) f(k, cells_.data() + k * card_);
+    } else {
+      for (const auto& [k, c] : sparse_) f(k, c.data());
+    }
   }
+  bool dense() const { return !cells_.empty() || r_ == 0; }
   std::vector<std::uint32_t>& cells() { return cells_; }
+  std::map<std::uint64_t, std::vector<std::uint32_t>>& sparse() { return sparse_; }
 
  private:
   std::uint64_t r_;
   int card_;
-  std::vector<std::uint32_t> cells_;
+  std::vector<std::uint32_t> cells_;  // dense storage (r * card <= 2^22)
+  std::map<std::uint64_t, std::vector<std::uint32_t>> sparse_;
 };
 
 CountTable count_statistics(const Dataset& data, int node, ParentSet pset);

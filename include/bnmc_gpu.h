@@ -24,7 +24,7 @@
  *
  * Conventions:
  *   * Every function returns a status: 0 ok, 2 usage (reference UsageError),
- *     3 data (DataError), 4 capacity (CapacityError), 5 CUDA, 1 other. The
+ *     3 data (DataError), 4 capacity (CapacityError), 5 CUDA, 6 NCCL, 1 other. The
  *     message of the last failure on the calling thread is returned by
  *     bnmc_gpu_last_error_message().
  *   * The caller owns every host buffer; the library owns device memory through
@@ -54,12 +54,14 @@ enum {
   BNMC_USAGE = 2,
   BNMC_DATA = 3,
   BNMC_CAPACITY = 4,
-  BNMC_CUDA = 5
+  BNMC_CUDA = 5,
+  BNMC_NCCL = 6
 };
 
 enum { BNMC_ALPHA_BDEU = 0, BNMC_ALPHA_K2 = 1 };
 
 typedef struct bnmc_table bnmc_table;
+typedef struct bnmc_comm bnmc_comm;
 
 /* The scoring fields of RunConfig (types.hpp:167-183) that the table depends on. */
 typedef struct {
@@ -68,7 +70,13 @@ typedef struct {
   double ess;                /* equivalent sample size, > 0 */
   int alpha_mode;            /* BNMC_ALPHA_BDEU | BNMC_ALPHA_K2 */
   uint64_t memory_cap_bytes; /* RunConfig::memory_cap_bytes (checked like estimate_bytes) */
-  int device;                /* CUDA ordinal this table lives on */
+  int device;                /* CUDA ordinal this table lives on (the first of n_gpus) */
+  int n_gpus;                /* 0 or 1: one device. G > 1: one process drives devices
+                                device .. device+G-1 — the precompute is split into G
+                                work-balanced parts (bnmc_gpu_k1_partition), one per
+                                GPU, combined by an NCCL all-reduce over NVLink; every
+                                GPU keeps a full replica and bnmc_gpu_run_chains spreads
+                                chains over them (contiguous blocks, chain order kept) */
 } bnmc_score_params;
 
 const char* bnmc_gpu_last_error_message(void);
@@ -102,6 +110,57 @@ int bnmc_gpu_table_build(const uint8_t* cells, const int* cards, uint64_t m, int
 int bnmc_gpu_table_build_rows(const uint8_t* cells, const int* cards, uint64_t m, int n,
                               const bnmc_score_params* params, const double* prior_r,
                               int row_begin, int row_end, bnmc_table** out);
+/* Work-balanced partition of the precompute into `nparts` parts (host only, no
+ * device needed). K1 works per prefix P (|P| <= s) in the global-index order of
+ * subsets of the n variables; part g owns prefix indices [cuts[g], cuts[g+1])
+ * (cuts: nparts + 1 values) and with them every entry (v, pi) whose joint set
+ * pi + {v} minus its largest member is such a prefix — the parts' entries are
+ * disjoint and cover the table. Replaces the reference's OpenMP row loop over
+ * nodes (src/scoring.cpp:179-190) as the unit of parallel work. */
+int bnmc_gpu_k1_partition(const int* cards, uint64_t m, int n, int s, int nparts,
+                          uint64_t* cuts);
+
+/* Multi-GPU precompute, one part per GPU: allocate the full table, zero it and
+ * compute the entries of part `part` of bnmc_gpu_k1_partition(nparts). The
+ * parts combine by an integer (bitwise-exact) sum of the 64-bit table words,
+ * e.g. ncclAllReduce(ncclInt64, ncclSum) over bnmc_gpu_table_rows_buffer, or
+ * bnmc_gpu_table_build_comm which does this internally; then
+ * bnmc_gpu_table_finalize. */
+int bnmc_gpu_table_build_part(const uint8_t* cells, const int* cards, uint64_t m, int n,
+                              const bnmc_score_params* params, const double* prior_r, int part,
+                              int nparts, bnmc_table** out);
+
+/* Multi-process multi-GPU (one process per GPU, e.g. under torchrun): an
+ * NCCL communicator over NVLink/NVSwitch. Rank 0 creates the unique id
+ * (NCCL_UNIQUE_ID_BYTES = 128 bytes) and ships it to the other ranks out of
+ * band (e.g. torch.distributed broadcast); every rank then calls
+ * bnmc_gpu_comm_init with its rank and CUDA device. Collective calls below
+ * must be made by every rank in the same order. NCCL is loaded at first use
+ * (libnccl.so.2; BNMC_NCCL_LIB overrides); failures are status 6. */
+int bnmc_gpu_comm_unique_id(uint8_t* id128);
+int bnmc_gpu_comm_init(const uint8_t* id128, int nranks, int rank, int device, bnmc_comm** out);
+int bnmc_gpu_comm_free(bnmc_comm* comm);
+/* ScoreCache::build over a communicator: rank r computes part r of nranks
+ * (bnmc_gpu_k1_partition), an in-place ncclAllReduce(int64, sum) of the table
+ * words completes it on every rank (bit-exact: each entry has one writer),
+ * then the PPF fold. params->device must be the communicator's device. */
+int bnmc_gpu_table_build_comm(const uint8_t* cells, const int* cards, uint64_t m, int n,
+                              const bnmc_score_params* params, const double* prior_r,
+                              bnmc_comm* comm, bnmc_table** out);
+/* All-gather of `bytes` of host data per rank (e.g. fixed-size chain records)
+ * through device buffers: recv receives nranks * bytes in rank order. */
+int bnmc_gpu_comm_allgather(bnmc_comm* comm, const void* send, uint64_t bytes, void* recv);
+/* Element-wise max over ranks of `count` doubles, in place (timings). */
+int bnmc_gpu_comm_allreduce_max(bnmc_comm* comm, double* values, int count);
+/* Devices a table spans (1 unless built with n_gpus > 1) and their ordinals. */
+int bnmc_gpu_table_devices(const bnmc_table* t, int* count, int* devices /* >= count */);
+
+/* Last precompute run on this table: K1 + K1W device time (ms), entries scored
+ * by the wide path (joint spaces beyond the dense counter) and the prefix
+ * index range computed. */
+int bnmc_gpu_table_k1_stats(const bnmc_table* t, float* k1_ms, uint64_t* wide_entries,
+                            uint64_t* prefix_lo, uint64_t* prefix_hi);
+
 /* Device pointer and byte size of the fp64 local-score rows (n x S doubles,
  * contiguous, row stride S). Valid until bnmc_gpu_table_free. */
 int bnmc_gpu_table_rows_buffer(bnmc_table* t, void** dev_ptr, uint64_t* bytes,
@@ -129,6 +188,17 @@ int bnmc_gpu_count_statistics(const uint8_t* cells, const int* cards, uint64_t m
                               int count, const int* nodes, const uint64_t* psets,
                               const uint64_t* offsets, uint32_t* out,
                               uint64_t* configs_out, int device);
+
+/* count_statistics as the reference's CountTable iterates it (for_each_active,
+ * scoring.hpp:55-67; dense or ordered-map storage, scoring.cpp:53-80): the
+ * active parent configurations of (node, pset) ascending, written to
+ * configs_out (capacity m), with their card(node) state counts in counts_out
+ * (capacity m * card(node)); *n_active receives their number. No limit on the
+ * configuration space other than the reference's 64-bit overflow check
+ * (status 4, "parent configuration space overflows 64 bits"). */
+int bnmc_gpu_count_statistics_sparse(const uint8_t* cells, const int* cards, uint64_t m, int n,
+                                     int node, uint64_t pset, uint64_t* configs_out,
+                                     uint32_t* counts_out, uint64_t* n_active, int device);
 
 /* OrderScorer::score for `count` orders (perms: count x n positions->node).
  * Outputs per order: parent masks (n, indexed by node), per-node effective

@@ -62,6 +62,12 @@ def lib():
     L.ref_shuffle_identity.argtypes = [C.c_int, C.c_uint64, C.c_int64, _i32p]
     L.ref_count_statistics.argtypes = [_u8p, _i32p, C.c_int, C.c_uint64, C.c_int, C.c_uint64,
                                        _u32p, C.c_uint64, C.POINTER(C.c_uint64)]
+    L.ref_count_statistics_active.argtypes = [_u8p, _i32p, C.c_int, C.c_uint64, C.c_int,
+                                              C.c_uint64, _u64p, _u32p, C.c_uint64,
+                                              C.POINTER(C.c_uint64)]
+    L.ref_local_score_batch.argtypes = [_u8p, _i32p, C.c_int, C.c_uint64, C.c_int, _i32p, _u64p,
+                                        C.c_double, C.c_double, C.c_int, _f64p,
+                                        C.POINTER(C.c_double)]
     L.ref_local_score.argtypes = [_u8p, _i32p, C.c_int, C.c_uint64, C.c_int, C.c_uint64,
                                   C.c_double, C.c_double, C.c_int, C.POINTER(C.c_double)]
     L.ref_ppf.argtypes = [C.c_double, C.POINTER(C.c_double)]
@@ -184,6 +190,21 @@ def count_statistics(cells, cards, node, pset, cap=1 << 22):
     return out[: r.value * int(cards[node])].reshape(r.value, int(cards[node]))
 
 
+def count_statistics_active(cells, cards, node, pset):
+    """(configs, counts) of CountTable::for_each_active (scoring.hpp:55-67)."""
+    cells = np.ascontiguousarray(cells, np.uint8)
+    m, n = cells.shape
+    cap = max(m, 1)
+    cv = int(cards[node])
+    cfg = np.zeros(cap, np.uint64)
+    cnt = np.zeros(cap * cv, np.uint32)
+    na = C.c_uint64()
+    _check(lib().ref_count_statistics_active(cells.ravel(), np.ascontiguousarray(cards, np.int32),
+                                             n, m, node, pset, cfg, cnt, cap, C.byref(na)))
+    k = na.value
+    return cfg[:k], cnt[:k * cv].reshape(k, cv)
+
+
 def local_score(cells, cards, node, pset, gamma=0.1, ess=1.0, k2=False):
     cells = np.ascontiguousarray(cells, np.uint8)
     m, n = cells.shape
@@ -191,6 +212,20 @@ def local_score(cells, cards, node, pset, gamma=0.1, ess=1.0, k2=False):
     _check(lib().ref_local_score(cells.ravel(), np.ascontiguousarray(cards, np.int32), n, m,
                                  node, pset, gamma, ess, int(k2), C.byref(out)))
     return out.value
+
+
+def local_score_batch(cells, cards, nodes, psets, gamma=0.1, ess=1.0, k2=False):
+    """(scores, seconds): local_score of many entries on one Dataset, one thread."""
+    cells = np.ascontiguousarray(cells, np.uint8)
+    m, n = cells.shape
+    nodes = np.ascontiguousarray(nodes, np.int32)
+    psets = np.ascontiguousarray(psets, np.uint64)
+    out = np.zeros(nodes.size, np.float64)
+    sec = C.c_double()
+    _check(lib().ref_local_score_batch(cells.ravel(), np.ascontiguousarray(cards, np.int32), n, m,
+                                       nodes.size, nodes, psets, gamma, ess, int(k2), out,
+                                       C.byref(sec)))
+    return out, sec.value
 
 
 def ppf(r):

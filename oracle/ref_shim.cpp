@@ -12,6 +12,7 @@
 
 #include <omp.h>
 
+#include <chrono>
 #include <cstdint>
 #include <cstring>
 #include <exception>
@@ -194,6 +195,26 @@ int ref_count_statistics(const std::uint8_t* cells, const int* cards, int n,
   });
 }
 
+// count_statistics as CountTable::for_each_active sees it (dense or map
+// storage): active configurations ascending with their state counts.
+int ref_count_statistics_active(const std::uint8_t* cells, const int* cards, int n,
+                                std::uint64_t m, int node, std::uint64_t pset,
+                                std::uint64_t* configs_out, std::uint32_t* counts_out,
+                                std::uint64_t cap, std::uint64_t* n_active) {
+  return guarded([&] {
+    const Dataset d = make_dataset(cells, cards, n, m);
+    const CountTable t = count_statistics(d, node, ParentSet{pset});
+    std::uint64_t k = 0;
+    t.for_each_active([&](std::uint64_t cfg, const std::uint32_t* row) {
+      if (k >= cap) throw CapacityError("more active configurations than the buffer holds");
+      configs_out[k] = cfg;
+      for (int j = 0; j < t.child_card(); ++j) counts_out[k * t.child_card() + j] = row[j];
+      ++k;
+    });
+    *n_active = k;
+  });
+}
+
 int ref_local_score(const std::uint8_t* cells, const int* cards, int n,
                     std::uint64_t m, int node, std::uint64_t pset, double gamma,
                     double ess, int k2, double* out) {
@@ -201,6 +222,21 @@ int ref_local_score(const std::uint8_t* cells, const int* cards, int n,
     const Dataset d = make_dataset(cells, cards, n, m);
     const Hyperparams hp{gamma, ess, k2 ? AlphaMode::kK2 : AlphaMode::kBdeu};
     *out = local_score(node, ParentSet{pset}, d, hp);
+  });
+}
+
+// local_score over `count` entries on one Dataset (built once, outside the
+// timed loop), single thread: the per-entry body of ScoreCache::build
+// (scoring.cpp:179-190). *seconds receives the loop's wall time.
+int ref_local_score_batch(const std::uint8_t* cells, const int* cards, int n, std::uint64_t m,
+                          int count, const int* nodes, const std::uint64_t* psets, double gamma,
+                          double ess, int k2, double* out, double* seconds) {
+  return guarded([&] {
+    const Dataset d = make_dataset(cells, cards, n, m);
+    const Hyperparams hp{gamma, ess, k2 ? AlphaMode::kK2 : AlphaMode::kBdeu};
+    const auto t0 = std::chrono::steady_clock::now();
+    for (int e = 0; e < count; ++e) out[e] = local_score(nodes[e], ParentSet{psets[e]}, d, hp);
+    *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   });
 }
 

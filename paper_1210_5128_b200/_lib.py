@@ -25,7 +25,8 @@ _vp = C.c_void_p
 
 class ScoreParams(C.Structure):
     _fields_ = [("max_parents", C.c_int), ("gamma", C.c_double), ("ess", C.c_double),
-                ("alpha_mode", C.c_int), ("memory_cap_bytes", C.c_uint64), ("device", C.c_int)]
+                ("alpha_mode", C.c_int), ("memory_cap_bytes", C.c_uint64), ("device", C.c_int),
+                ("n_gpus", C.c_int)]
 
 
 class ChainParams(C.Structure):
@@ -80,6 +81,23 @@ SIGNATURES = {
                                              C.POINTER(C.c_int)]),
     "bnmc_gpu_bench_scan": (C.c_int, [_vp, _i32p, C.c_int, C.c_int, C.c_int, C.c_int,
                                       C.POINTER(C.c_float)]),
+    "bnmc_gpu_k1_partition": (C.c_int, [_i32p, C.c_uint64, C.c_int, C.c_int, C.c_int, _u64p]),
+    "bnmc_gpu_table_build_part": (C.c_int, [_u8p, _i32p, C.c_uint64, C.c_int,
+                                            C.POINTER(ScoreParams), _vp, C.c_int, C.c_int,
+                                            C.POINTER(_vp)]),
+    "bnmc_gpu_table_k1_stats": (C.c_int, [_vp, C.POINTER(C.c_float), C.POINTER(C.c_uint64),
+                                          C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
+    "bnmc_gpu_count_statistics_sparse": (C.c_int, [_u8p, _i32p, C.c_uint64, C.c_int, C.c_int,
+                                                   C.c_uint64, _u64p, _u32p,
+                                                   C.POINTER(C.c_uint64), C.c_int]),
+    "bnmc_gpu_comm_unique_id": (C.c_int, [_u8p]),
+    "bnmc_gpu_comm_init": (C.c_int, [_u8p, C.c_int, C.c_int, C.c_int, C.POINTER(_vp)]),
+    "bnmc_gpu_comm_free": (C.c_int, [_vp]),
+    "bnmc_gpu_table_build_comm": (C.c_int, [_u8p, _i32p, C.c_uint64, C.c_int,
+                                            C.POINTER(ScoreParams), _vp, _vp, C.POINTER(_vp)]),
+    "bnmc_gpu_comm_allgather": (C.c_int, [_vp, _vp, C.c_uint64, _vp]),
+    "bnmc_gpu_comm_allreduce_max": (C.c_int, [_vp, _f64p, C.c_int]),
+    "bnmc_gpu_table_devices": (C.c_int, [_vp, C.POINTER(C.c_int), _i32p]),
     "bnmc_synth_last_error": (C.c_char_p, []),
     "bnmc_synth_instance": (C.c_int, [C.c_int, C.c_int, C.c_double, C.c_double, C.c_uint64,
                                       _i32p, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64,
@@ -108,7 +126,11 @@ class CudaError(Error):
     """CUDA runtime failure or no usable sm_100 device (status 5)."""
 
 
-_EXC = {2: UsageError, 3: DataError, 4: CapacityError, 5: CudaError}
+class NcclError(Error):
+    """NCCL missing or a collective failed (status 6)."""
+
+
+_EXC = {2: UsageError, 3: DataError, 4: CapacityError, 5: CudaError, 6: NcclError}
 
 _lib = None
 

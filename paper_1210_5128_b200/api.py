@@ -49,6 +49,7 @@ class RunConfig:
     memory_cap_bytes: int = 4 << 30
     debug_recheck: bool = False
     device: int = 0
+    n_gpus: int = 1  # >1: one process drives devices device..device+n_gpus-1 (split K1, replicas)
     scan_mode: int = 0  # 0 auto (= 2), 1 full-row fp32-key scan (<= 64 chains), 2 sorted walk
     team_warps: int = 0  # sorted walk: warps per chain (0 auto, 1, 2, 4, 8)
     exact_accept: int = 0  # 0 device log10 + exact replay of ambiguous chains, 1 host glibc
@@ -73,7 +74,8 @@ class RunConfig:
 
     def score_params(self) -> _lib.ScoreParams:
         return _lib.ScoreParams(self.max_parents, self.gamma, self.ess, int(self.alpha_mode),
-                                min(self.memory_cap_bytes, (1 << 64) - 1), self.device)
+                                min(self.memory_cap_bytes, (1 << 64) - 1), self.device,
+                                self.n_gpus)
 
 
 class Dataset:
@@ -238,6 +240,86 @@ def read_bnsc(path, cfg: RunConfig):
         if len(body) < 8 * n * per:
             raise DataError(f"cache file truncated: {path}")
         return n, s, np.frombuffer(body, dtype="<f8").astype(np.float64).reshape(n, per)
+
+
+# -------------------------------------------------------------- CountTable
+_DENSE_CELLS = 1 << 22  # scoring.cpp:13
+
+
+class CountTable:
+    """CountTable (scoring.hpp:41-77): N_ijk of one (node, parent set), dense
+    (configs x card) up to 2^22 cells, else the active configurations only —
+    iteration ascending either way (for_each_active)."""
+
+    def __init__(self, configs, card, dense=None, active=None, counts=None):
+        self._r, self._card = configs, card
+        self._dense = dense
+        self._active = active
+        self._counts = counts
+
+    def configs(self):
+        return self._r
+
+    def child_card(self):
+        return self._card
+
+    def is_dense(self):
+        return self._dense is not None
+
+    def samples(self):
+        return int(self._dense.sum() if self._dense is not None else self._counts.sum())
+
+    def njk(self, config, state):
+        if self._dense is not None:
+            return int(self._dense[config, state])
+        i = int(np.searchsorted(self._active, np.uint64(config)))
+        if i < self._active.size and int(self._active[i]) == config:
+            return int(self._counts[i, state])
+        return 0
+
+    def nk(self, config):
+        return sum(self.njk(config, j) for j in range(self._card))
+
+    def for_each_active(self):
+        """(config, counts row) for every config with N_ik > 0, ascending."""
+        if self._dense is not None:
+            for k in np.nonzero(self._dense.sum(axis=1))[0]:
+                yield int(k), self._dense[k]
+        else:
+            for k, row in zip(self._active, self._counts):
+                yield int(k), row
+
+
+def count_statistics(data, node, pset, device=0):
+    """count_statistics (scoring.cpp:82-109) on the device."""
+    n, m = data.n, data.rows()
+    if not 0 <= node < n or (n < 64 and pset >> n):
+        raise UsageError("count_statistics: bad (node, parent set)")
+    if pset >> node & 1:
+        raise DataError("node cannot appear in its own parent set")
+    r = 1
+    for p in range(n):
+        if pset >> p & 1:
+            r *= int(data.cards[p])
+    if r >= 1 << 64:
+        raise CapacityError("parent configuration space overflows 64 bits")
+    card = int(data.cards[node])
+    cells = np.ascontiguousarray(data.cells).reshape(-1)
+    if r * card <= _DENSE_CELLS:
+        out = np.zeros(r * card, np.uint32)
+        cfgs = np.zeros(1, np.uint64)
+        _lib.check(_lib.lib().bnmc_gpu_count_statistics(
+            cells, data.cards, m, n, 1, np.array([node], np.int32), np.array([pset], np.uint64),
+            np.zeros(1, np.uint64), out, cfgs, device))
+        return CountTable(r, card, dense=out.reshape(r, card))
+    cap = max(m, 1)
+    act = np.zeros(cap, np.uint64)
+    cnt = np.zeros(cap * card, np.uint32)
+    na = C.c_uint64()
+    _lib.check(_lib.lib().bnmc_gpu_count_statistics_sparse(cells, data.cards, m, n, node, pset,
+                                                            act, cnt, C.byref(na), device))
+    k = na.value
+    return CountTable(r, card, active=act[:k].copy(), counts=cnt[:k * card].reshape(k, card).copy())
 
 
 # -------------------------------------------------------------- ScoreCache

@@ -17,6 +17,7 @@
 #include <memory>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/bnmc_gpu.h"
@@ -27,12 +28,15 @@
 #include "common.cuh"
 #include "host_util.hpp"
 #include "precompute.cuh"
+#include "nccl_dyn.hpp"
 
 using namespace bnmc_dev;
 using bnmc_host::raise;
 using bnmc_host::Status;
 using bnmc_host::cuda_check;
-using bnmc_host::precompute_rows;
+using bnmc_host::precompute;
+using bnmc_host::K1Range;
+using bnmc_host::K1Report;
 using bnmc_host::count_statistics_device;
 
 namespace {
@@ -105,6 +109,7 @@ void validate_params(const bnmc_score_params* p) {
   if (!(p->ess > 0.0)) raise(BNMC_USAGE, "ess must be positive");
   if (p->alpha_mode != BNMC_ALPHA_BDEU && p->alpha_mode != BNMC_ALPHA_K2)
     raise(BNMC_USAGE, "alpha_mode must be BDeu (0) or K2 (1)");
+  if (p->n_gpus < 0 || p->n_gpus > 64) raise(BNMC_USAGE, "n_gpus must lie in [0,64]");
 }
 
 // ppf (scoring.cpp:143-148) and PpfTable (scoring.cpp:150-155).
@@ -142,6 +147,17 @@ struct DevBuf {
 };
 
 }  // namespace
+
+// One rank of a multi-process NCCL communicator (bnmc_gpu_comm_init).
+struct bnmc_comm {
+  ncclComm_t comm = nullptr;
+  int rank = 0, nranks = 1, dev = 0;
+  cudaStream_t stream = nullptr;
+  ~bnmc_comm() {
+    if (comm) bnmc_host::nccl().CommDestroy(comm);
+    if (stream) cudaStreamDestroy(stream);
+  }
+};
 
 static uint64_t env_u64(const char* name, uint64_t dflt) {
   const char* e = std::getenv(name);
@@ -189,6 +205,7 @@ struct bnmc_table {
   DevBuf<unsigned long long> d_acc;
   DevBuf<double> d_fs;
   float build_ms = 0.f, fold_ms = 0.f;
+  uint64_t wide_entries = 0, p_lo = 0, p_hi = 0;  // last K1 run (stats)
   // chain / order-scoring workspace
   DevBuf<ChainState> st;
   DevBuf<Item> items;
@@ -217,7 +234,14 @@ struct bnmc_table {
   DevBuf<int> d_amb;
   float last_scan_ms = 0.f, last_total_ms = 0.f;
   int last_G = 0;
+  // Multi-GPU table (n_gpus > 1): full replicas on the other devices, owned.
+  std::vector<bnmc_table*> replicas;
   ~bnmc_table() {
+    for (bnmc_table* r : replicas) {
+      cudaSetDevice(r->dev);
+      delete r;
+    }
+    cudaSetDevice(dev);
     if (stream) cudaStreamDestroy(stream);
   }
 };
@@ -1002,6 +1026,184 @@ void run_chains_walk(bnmc_table* t, const uint64_t* seeds, int C, const bnmc_cha
   t->last_launches = 2;
 }
 
+void validate_cards(const int* cards, int n) {
+  for (int i = 0; i < n; ++i)
+    if (cards[i] < 2 || cards[i] > 256)
+      raise(BNMC_DATA, "cardinality of variable " + std::to_string(i) + " out of range [2,256]");
+}
+
+// Dataset validation (types.cpp:8-26).
+void validate_dataset(const uint8_t* cells, const int* cards, uint64_t m, int n) {
+  if (n < 1 || n > 64) raise(BNMC_DATA, "dataset must have between 1 and 64 variables");
+  validate_cards(cards, n);
+  for (uint64_t r = 0; r < m; ++r)
+    for (int i = 0; i < n; ++i)
+      if (cells[r * n + i] >= cards[i])
+        raise(BNMC_DATA, "state out of range at row " + std::to_string(r) + ", column " +
+                             std::to_string(i));
+}
+
+// K1 (+ K1W) for a prefix / row range of the table's local scores.
+void run_k1(bnmc_table* t, const uint8_t* cells, const int* cards, uint64_t m, const K1Range& R) {
+  K1Report rep;
+  precompute(t->stream, t->ls.p, t->S, cells, cards, m, t->n, t->s, t->gamma, t->ess, t->alpha, R,
+             &rep);
+  t->build_ms = rep.ms;
+  t->wide_entries = rep.wide_entries;
+  const uint64_t total = bnmc_host::prefix_total(t->n, t->s);
+  t->p_lo = std::min(R.p_lo, total);
+  t->p_hi = std::min(R.p_hi, total);
+}
+
+template <class F>
+void for_each_replica(bnmc_table* t, F&& f) {
+  f(t);
+  for (bnmc_table* r : t->replicas) f(r);
+}
+
+// Run f(g) on one host thread per device g (each thread binds its device);
+// the first exception is rethrown on the caller's thread.
+template <class F>
+void on_devices(const std::vector<bnmc_table*>& ts, F&& f) {
+  if (ts.size() == 1) {
+    CK(cudaSetDevice(ts[0]->dev));
+    f(0);
+    return;
+  }
+  std::vector<std::exception_ptr> errs(ts.size());
+  std::vector<std::thread> th;
+  for (size_t g = 0; g < ts.size(); ++g)
+    th.emplace_back([&, g] {
+      try {
+        CK(cudaSetDevice(ts[g]->dev));
+        f(static_cast<int>(g));
+      } catch (...) {
+        errs[g] = std::current_exception();
+      }
+    });
+  for (auto& x : th) x.join();
+  for (auto& e : errs)
+    if (e) std::rethrow_exception(e);
+}
+
+// Devices of an n_gpus table: device .. device+G-1. BNMC_DEVICES="a,b,..."
+// overrides the list (development: several parts on one GPU).
+std::vector<int> device_list(int first, int G) {
+  std::vector<int> d;
+  if (const char* e = std::getenv("BNMC_DEVICES")) {
+    for (const char* p = e; *p;) {
+      d.push_back(static_cast<int>(std::strtol(p, const_cast<char**>(&p), 10)));
+      while (*p == ',' || *p == ' ') ++p;
+    }
+    if (static_cast<int>(d.size()) < G) raise(BNMC_USAGE, "BNMC_DEVICES lists fewer than n_gpus devices");
+    d.resize(G);
+    return d;
+  }
+  int count = 0;
+  CK(cudaGetDeviceCount(&count));
+  if (first + G > count)
+    raise(BNMC_CUDA, std::to_string(G) + " GPUs requested from device " + std::to_string(first) +
+                         ", " + std::to_string(count) + " visible");
+  for (int g = 0; g < G; ++g) d.push_back(first + g);
+  return d;
+}
+
+__global__ void add_i64_kernel(unsigned long long* __restrict__ dst,
+                               const unsigned long long* __restrict__ src, uint64_t count) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    dst[i] += src[i];
+}
+
+// Complete a table from its parts: every local-score word is written by
+// exactly one part and zero elsewhere, so an integer sum of the 64-bit words
+// is the bitwise union. Distinct devices: ncclAllReduce(int64, sum) in place
+// over NVLink (one group call). Shared devices (BNMC_DEVICES): peer copies +
+// an add kernel on the first table, then copies back.
+void combine_parts(const std::vector<bnmc_table*>& ts) {
+  const size_t words = static_cast<size_t>(ts[0]->n) * ts[0]->S;
+  bool distinct = true;
+  for (size_t i = 0; i < ts.size(); ++i)
+    for (size_t j = 0; j < i; ++j) distinct &= ts[i]->dev != ts[j]->dev;
+  if (distinct) {
+    const auto& N = bnmc_host::nccl();
+    std::vector<int> devs;
+    for (auto* t : ts) devs.push_back(t->dev);
+    std::vector<ncclComm_t> comms(ts.size());
+    NK(N.CommInitAll(comms.data(), static_cast<int>(ts.size()), devs.data()));
+    NK(N.GroupStart());
+    for (size_t g = 0; g < ts.size(); ++g) {
+      CK(cudaSetDevice(ts[g]->dev));
+      NK(N.AllReduce(ts[g]->ls.p, ts[g]->ls.p, words, ncclInt64, ncclSum, comms[g], ts[g]->stream));
+    }
+    NK(N.GroupEnd());
+    for (size_t g = 0; g < ts.size(); ++g) {
+      CK(cudaSetDevice(ts[g]->dev));
+      CK(cudaStreamSynchronize(ts[g]->stream));
+      N.CommDestroy(comms[g]);
+    }
+    CK(cudaSetDevice(ts[0]->dev));
+    return;
+  }
+  bnmc_table* t0 = ts[0];
+  CK(cudaSetDevice(t0->dev));
+  DevBuf<unsigned long long> tmp;
+  tmp.alloc(words);
+  auto* dst = reinterpret_cast<unsigned long long*>(t0->ls.p);
+  for (size_t g = 1; g < ts.size(); ++g) {
+    CK(cudaMemcpyPeerAsync(tmp.p, t0->dev, ts[g]->ls.p, ts[g]->dev, words * 8, t0->stream));
+    add_i64_kernel<<<148 * 8, 256, 0, t0->stream>>>(dst, tmp.p, words);
+    CK(cudaGetLastError());
+  }
+  for (size_t g = 1; g < ts.size(); ++g)
+    CK(cudaMemcpyPeerAsync(ts[g]->ls.p, ts[g]->dev, t0->ls.p, t0->dev, words * 8, t0->stream));
+  CK(cudaStreamSynchronize(t0->stream));
+}
+
+// ScoreCache::build over G devices of this process (bnmc_score_params::n_gpus).
+bnmc_table* build_multi(const uint8_t* cells, const int* cards, uint64_t m, int n,
+                        const bnmc_score_params* params, const double* prior_r) {
+  const int G = params->n_gpus;
+  const std::vector<int> devs = device_list(params->device, G);
+  std::vector<std::unique_ptr<bnmc_table>> own;
+  std::vector<bnmc_table*> ts;
+  for (int g = 0; g < G; ++g) {
+    bnmc_score_params p = *params;
+    p.device = devs[g];
+    p.n_gpus = 1;
+    own.emplace_back(new bnmc_table);
+    table_init(own.back().get(), n, &p);
+    set_priors(own.back().get(), prior_r);
+    CK(cudaMemsetAsync(own.back()->ls.p, 0, static_cast<size_t>(n) * own.back()->S * 8,
+                       own.back()->stream));
+    ts.push_back(own.back().get());
+  }
+  const std::vector<uint64_t> cut = bnmc_host::k1_partition(cards, n, params->max_parents, m, G);
+  on_devices(ts, [&](int g) {
+    K1Range R;
+    R.p_lo = cut[g];
+    R.p_hi = cut[g + 1];
+    run_k1(ts[g], cells, cards, m, R);
+    CK(cudaStreamSynchronize(ts[g]->stream));
+  });
+  combine_parts(ts);
+  on_devices(ts, [&](int g) { fold(ts[g]); });
+  bnmc_table* t = own[0].release();
+  float k1 = t->build_ms;
+  uint64_t wide = t->wide_entries;
+  for (int g = 1; g < G; ++g) {
+    k1 = std::max(k1, own[g]->build_ms);
+    wide += own[g]->wide_entries;
+    t->replicas.push_back(own[g].release());
+  }
+  t->build_ms = k1;  // the slowest part
+  t->wide_entries = wide;
+  t->p_lo = 0;
+  t->p_hi = cut[G];
+  CK(cudaSetDevice(t->dev));
+  return t;
+}
+
 int read_error(bnmc_table* t) {
   int err = 0;
   CK(cudaMemcpy(&err, t->rowcnt.p + 2 * t->n + 1, sizeof(int), cudaMemcpyDeviceToHost));
@@ -1074,6 +1276,13 @@ int bnmc_gpu_table_upload(const double* table, int n, const bnmc_score_params* p
 int bnmc_gpu_table_build(const uint8_t* cells, const int* cards, uint64_t m, int n,
                          const bnmc_score_params* params, const double* prior_r,
                          bnmc_table** out) {
+  if (params && params->n_gpus > 1)
+    return guarded([&] {
+      *out = nullptr;
+      validate_params(params);
+      validate_dataset(cells, cards, m, n);
+      *out = build_multi(cells, cards, m, n, params, prior_r);
+    });
   int st = bnmc_gpu_table_build_rows(cells, cards, m, n, params, prior_r, 0, n, out);
   if (st != BNMC_OK) return st;
   st = bnmc_gpu_table_finalize(*out);
@@ -1091,22 +1300,60 @@ int bnmc_gpu_table_build_rows(const uint8_t* cells, const int* cards, uint64_t m
                               int row_begin, int row_end, bnmc_table** out) {
   return guarded([&] {
     *out = nullptr;
-    if (n < 1 || n > 64) raise(BNMC_DATA, "dataset must have between 1 and 64 variables");
-    for (int i = 0; i < n; ++i)
-      if (cards[i] < 2 || cards[i] > 256)
-        raise(BNMC_DATA, "cardinality of variable " + std::to_string(i) + " out of range [2,256]");
-    for (uint64_t r = 0; r < m; ++r)
-      for (int i = 0; i < n; ++i)
-        if (cells[r * n + i] >= cards[i])
-          raise(BNMC_DATA, "state out of range at row " + std::to_string(r) + ", column " +
-                               std::to_string(i));
+    validate_dataset(cells, cards, m, n);
     if (row_begin < 0 || row_end > n || row_begin > row_end) raise(BNMC_USAGE, "bad row range");
     auto t = std::make_unique<bnmc_table>();
     table_init(t.get(), n, params);
     set_priors(t.get(), prior_r);
-    precompute_rows(t->stream, t->ls.p, t->S, cells, cards, m, n, t->s, t->gamma, t->ess,
-                    t->alpha, row_begin, row_end, &t->build_ms);
+    K1Range R;
+    R.row_begin = row_begin;
+    R.row_end = row_end;
+    run_k1(t.get(), cells, cards, m, R);
     *out = t.release();
+  });
+}
+
+int bnmc_gpu_k1_partition(const int* cards, uint64_t m, int n, int s, int nparts,
+                          uint64_t* cuts) {
+  return guarded([&] {
+    if (n < 1 || n > 64) raise(BNMC_DATA, "dataset must have between 1 and 64 variables");
+    if (s < 0 || s > 8) raise(BNMC_USAGE, "max-parents must lie in [0,8]");
+    if (nparts < 1) raise(BNMC_USAGE, "nparts must be >= 1");
+    validate_cards(cards, n);
+    const std::vector<uint64_t> c = bnmc_host::k1_partition(cards, n, s, m, nparts);
+    std::copy(c.begin(), c.end(), cuts);
+  });
+}
+
+int bnmc_gpu_table_build_part(const uint8_t* cells, const int* cards, uint64_t m, int n,
+                              const bnmc_score_params* params, const double* prior_r, int part,
+                              int nparts, bnmc_table** out) {
+  return guarded([&] {
+    *out = nullptr;
+    validate_dataset(cells, cards, m, n);
+    if (nparts < 1 || part < 0 || part >= nparts) raise(BNMC_USAGE, "bad part index");
+    auto t = std::make_unique<bnmc_table>();
+    table_init(t.get(), n, params);
+    set_priors(t.get(), prior_r);
+    const std::vector<uint64_t> cut =
+        bnmc_host::k1_partition(cards, n, t->s, m, nparts);
+    CK(cudaMemsetAsync(t->ls.p, 0, static_cast<size_t>(n) * t->S * 8, t->stream));
+    K1Range R;
+    R.p_lo = cut[part];
+    R.p_hi = cut[part + 1];
+    run_k1(t.get(), cells, cards, m, R);
+    *out = t.release();
+  });
+}
+
+int bnmc_gpu_table_k1_stats(const bnmc_table* t, float* k1_ms, uint64_t* wide_entries,
+                            uint64_t* prefix_lo, uint64_t* prefix_hi) {
+  return guarded([&] {
+    if (!t) raise(BNMC_USAGE, "null table");
+    if (k1_ms) *k1_ms = t->build_ms;
+    if (wide_entries) *wide_entries = t->wide_entries;
+    if (prefix_lo) *prefix_lo = t->p_lo;
+    if (prefix_hi) *prefix_hi = t->p_hi;
   });
 }
 
@@ -1131,9 +1378,119 @@ int bnmc_gpu_table_finalize(bnmc_table* t) {
 int bnmc_gpu_table_set_priors(bnmc_table* t, const double* prior_r) {
   return guarded([&] {
     if (!t) raise(BNMC_USAGE, "null table");
+    for_each_replica(t, [&](bnmc_table* r) {
+      CK(cudaSetDevice(r->dev));
+      set_priors(r, prior_r);
+      fold(r);
+    });
     CK(cudaSetDevice(t->dev));
-    set_priors(t, prior_r);
-    fold(t);
+  });
+}
+
+// ------------------------------------------------------------ communicators
+int bnmc_gpu_comm_unique_id(uint8_t* id128) {
+  return guarded([&] {
+    if (!id128) raise(BNMC_USAGE, "null id buffer");
+    static_assert(sizeof(ncclUniqueId) == 128, "NCCL unique id size");
+    ncclUniqueId id;
+    NK(bnmc_host::nccl().GetUniqueId(&id));
+    std::memcpy(id128, &id, sizeof(id));
+  });
+}
+
+int bnmc_gpu_comm_init(const uint8_t* id128, int nranks, int rank, int device, bnmc_comm** out) {
+  return guarded([&] {
+    *out = nullptr;
+    if (!id128) raise(BNMC_USAGE, "null id");
+    if (nranks < 1 || rank < 0 || rank >= nranks) raise(BNMC_USAGE, "bad rank / nranks");
+    ensure_device(device);
+    const auto& N = bnmc_host::nccl();
+    auto c = std::make_unique<bnmc_comm>();
+    c->rank = rank;
+    c->nranks = nranks;
+    c->dev = device;
+    ncclUniqueId id;
+    std::memcpy(&id, id128, sizeof(id));
+    NK(N.CommInitRank(&c->comm, nranks, id, rank));
+    CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    *out = c.release();
+  });
+}
+
+int bnmc_gpu_comm_free(bnmc_comm* c) {
+  return guarded([&] {
+    if (!c) return;
+    cudaSetDevice(c->dev);
+    delete c;
+  });
+}
+
+int bnmc_gpu_table_build_comm(const uint8_t* cells, const int* cards, uint64_t m, int n,
+                              const bnmc_score_params* params, const double* prior_r,
+                              bnmc_comm* comm, bnmc_table** out) {
+  return guarded([&] {
+    *out = nullptr;
+    if (!comm) raise(BNMC_USAGE, "null communicator");
+    validate_params(params);
+    if (params->device != comm->dev)
+      raise(BNMC_USAGE, "params->device must be the communicator's device");
+    validate_dataset(cells, cards, m, n);
+    auto t = std::make_unique<bnmc_table>();
+    table_init(t.get(), n, params);
+    set_priors(t.get(), prior_r);
+    const size_t words = static_cast<size_t>(n) * t->S;
+    CK(cudaMemsetAsync(t->ls.p, 0, words * 8, t->stream));
+    const std::vector<uint64_t> cut =
+        bnmc_host::k1_partition(cards, n, t->s, m, comm->nranks);
+    K1Range R;
+    R.p_lo = cut[comm->rank];
+    R.p_hi = cut[comm->rank + 1];
+    run_k1(t.get(), cells, cards, m, R);
+    // every word has one writer (zero elsewhere): the int64 sum is the union
+    NK(bnmc_host::nccl().AllReduce(t->ls.p, t->ls.p, words, ncclInt64, ncclSum, comm->comm,
+                                   t->stream));
+    CK(cudaStreamSynchronize(t->stream));
+    fold(t.get());
+    *out = t.release();
+  });
+}
+
+int bnmc_gpu_comm_allgather(bnmc_comm* c, const void* send, uint64_t bytes, void* recv) {
+  return guarded([&] {
+    if (!c) raise(BNMC_USAGE, "null communicator");
+    CK(cudaSetDevice(c->dev));
+    DevBuf<uint8_t> d;
+    d.alloc(bytes * (c->nranks + 1) + 1);
+    uint8_t* dsend = d.p + bytes * c->nranks;
+    CK(cudaMemcpyAsync(dsend, send, bytes, cudaMemcpyHostToDevice, c->stream));
+    NK(bnmc_host::nccl().AllGather(dsend, d.p, bytes, ncclUint8, c->comm, c->stream));
+    CK(cudaMemcpyAsync(recv, d.p, bytes * c->nranks, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int bnmc_gpu_comm_allreduce_max(bnmc_comm* c, double* values, int count) {
+  return guarded([&] {
+    if (!c) raise(BNMC_USAGE, "null communicator");
+    if (count < 1) return;
+    CK(cudaSetDevice(c->dev));
+    DevBuf<double> d;
+    d.alloc(count);
+    CK(cudaMemcpyAsync(d.p, values, 8ull * count, cudaMemcpyHostToDevice, c->stream));
+    NK(bnmc_host::nccl().AllReduce(d.p, d.p, count, ncclFloat64, ncclMax, c->comm, c->stream));
+    CK(cudaMemcpyAsync(values, d.p, 8ull * count, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int bnmc_gpu_table_devices(const bnmc_table* t, int* count, int* devices) {
+  return guarded([&] {
+    if (!t) raise(BNMC_USAGE, "null table");
+    if (count) *count = 1 + static_cast<int>(t->replicas.size());
+    if (devices) {
+      devices[0] = t->dev;
+      for (size_t g = 0; g < t->replicas.size(); ++g) devices[g + 1] = t->replicas[g]->dev;
+    }
   });
 }
 
@@ -1178,6 +1535,16 @@ int bnmc_gpu_count_statistics(const uint8_t* cells, const int* cards, uint64_t m
   return guarded([&] {
     ensure_device(device);
     count_statistics_device(cells, cards, m, n, count, nodes, psets, offsets, out, configs_out);
+  });
+}
+
+int bnmc_gpu_count_statistics_sparse(const uint8_t* cells, const int* cards, uint64_t m, int n,
+                                     int node, uint64_t pset, uint64_t* configs_out,
+                                     uint32_t* counts_out, uint64_t* n_active, int device) {
+  return guarded([&] {
+    ensure_device(device);
+    bnmc_host::count_statistics_sparse_device(cells, cards, m, n, node, pset, configs_out,
+                                              counts_out, n_active);
   });
 }
 
@@ -1276,12 +1643,62 @@ int bnmc_gpu_score_order(bnmc_table* t, const int* perm, uint64_t* masks_out, do
   return bnmc_gpu_score_orders(t, perm, 1, masks_out, best_out, total_out);
 }
 
+void run_chains_one(bnmc_table* t, const uint64_t* seeds, int n_chains,
+                    const bnmc_chain_params* params, double* trace_proposed,
+                    uint8_t* trace_accepted, double* trace_best, int* final_order,
+                    double* final_score, uint64_t* accepted, int* tracker_count,
+                    uint64_t* tracker_masks, double* tracker_totals, float* device_ms);
+
 int bnmc_gpu_run_chains(bnmc_table* t, const uint64_t* seeds, int n_chains,
                         const bnmc_chain_params* params, double* trace_proposed,
                         uint8_t* trace_accepted, double* trace_best, int* final_order,
                         double* final_score, uint64_t* accepted, int* tracker_count,
                         uint64_t* tracker_masks, double* tracker_totals, float* device_ms) {
   return guarded([&] {
+    if (!t) raise(BNMC_USAGE, "null table");
+    if (!params) raise(BNMC_USAGE, "null chain params");
+    if (t->replicas.empty() || n_chains < 2 || params->scan_mode == 1) {
+      run_chains_one(t, seeds, n_chains, params, trace_proposed, trace_accepted, trace_best,
+                     final_order, final_score, accepted, tracker_count, tracker_masks,
+                     tracker_totals, device_ms);
+      return;
+    }
+    // Multi-GPU table: contiguous chain blocks per device, outputs written in
+    // place (chain order preserved); device time = the slowest device.
+    std::vector<bnmc_table*> ts{t};
+    for (bnmc_table* r : t->replicas) ts.push_back(r);
+    const int G = static_cast<int>(std::min<size_t>(ts.size(), n_chains));
+    ts.resize(G);
+    const uint64_t I = params->iterations;
+    const int n = t->n, K = params->track_top;
+    std::vector<float> ms(G, 0.f);
+    on_devices(ts, [&](int g) {
+      const int c0 = static_cast<int>(static_cast<int64_t>(n_chains) * g / G);
+      const int c1 = static_cast<int>(static_cast<int64_t>(n_chains) * (g + 1) / G);
+      auto off = [&](auto* p, uint64_t per) { return p ? p + static_cast<uint64_t>(c0) * per : p; };
+      run_chains_one(ts[g], seeds + c0, c1 - c0, params, off(trace_proposed, I),
+                     off(trace_accepted, I), off(trace_best, I), off(final_order, n),
+                     off(final_score, 1), off(accepted, 1), off(tracker_count, 1),
+                     off(tracker_masks, static_cast<uint64_t>(K) * n), off(tracker_totals, K),
+                     &ms[g]);
+    });
+    CK(cudaSetDevice(t->dev));
+    if (device_ms) *device_ms = *std::max_element(ms.begin(), ms.end());
+    for (int g = 1; g < G; ++g) {  // walk statistics of the whole call on the primary
+      t->last_walked += ts[g]->last_walked;
+      t->last_enumerated += ts[g]->last_enumerated;
+      t->last_rescans += ts[g]->last_rescans;
+      t->last_replayed += ts[g]->last_replayed;
+    }
+  });
+}
+
+void run_chains_one(bnmc_table* t, const uint64_t* seeds, int n_chains,
+                    const bnmc_chain_params* params, double* trace_proposed,
+                    uint8_t* trace_accepted, double* trace_best, int* final_order,
+                    double* final_score, uint64_t* accepted, int* tracker_count,
+                    uint64_t* tracker_masks, double* tracker_totals, float* device_ms) {
+  {
     if (!t) raise(BNMC_USAGE, "null table");
     if (!params) raise(BNMC_USAGE, "null chain params");
     if (params->iterations < 1) raise(BNMC_USAGE, "iterations must be >= 1");
@@ -1442,7 +1859,7 @@ int bnmc_gpu_run_chains(bnmc_table* t, const uint64_t* seeds, int n_chains,
     t->last_scan_ms = scan_samples ? static_cast<float>(scan_ms / scan_samples) : 0.f;
     t->last_scan_samples = scan_samples;
     t->last_G = g.G;
-  });
+  }
 }
 
 int bnmc_gpu_scan_slice(bnmc_table* t, const int* perm, int position, uint64_t lo, uint64_t hi,
@@ -1481,7 +1898,7 @@ int bnmc_gpu_table_set_scan_mode(bnmc_table* t, int mode) {
   return guarded([&] {
     if (!t) raise(BNMC_USAGE, "null table");
     if (mode < 0 || mode > 2) raise(BNMC_USAGE, "scan_mode must be 0, 1 or 2");
-    t->scan_mode = mode;
+    for_each_replica(t, [&](bnmc_table* r) { r->scan_mode = mode; });
   });
 }
 
@@ -1489,21 +1906,26 @@ int bnmc_gpu_table_set_walk_cap(bnmc_table* t, int64_t walk_cap, int64_t budget,
   return guarded([&] {
     if (!t) raise(BNMC_USAGE, "null table");
     if (deep < -1 || deep > 1) raise(BNMC_USAGE, "deep must be -1, 0 or 1");
-    t->walk_deep = deep;
     if (budget > 0xFFFF) raise(BNMC_USAGE, "walk budget must be <= 65535");
-    t->walk_cap = walk_cap < 0 ? 0 : static_cast<uint64_t>(walk_cap);
-    t->walk_budget = budget < 0 ? static_cast<uint32_t>(kWalkBudget) : static_cast<uint32_t>(budget);
-    t->pst_ready = false;
+    for_each_replica(t, [&](bnmc_table* r) {
+      r->walk_deep = deep;
+      r->walk_cap = walk_cap < 0 ? 0 : static_cast<uint64_t>(walk_cap);
+      r->walk_budget =
+          budget < 0 ? static_cast<uint32_t>(kWalkBudget) : static_cast<uint32_t>(budget);
+      r->pst_ready = false;
+    });
   });
 }
 
 int bnmc_gpu_table_set_walk_params(bnmc_table* t, int64_t enum_max, int ylists) {
   return guarded([&] {
     if (!t) raise(BNMC_USAGE, "null table");
-    t->enum_max = enum_max < 0 ? kEnumMax : static_cast<uint64_t>(enum_max);
-    t->pst_ready = false;
-    t->ylist_mode = ylists;
-    t->sorted_valid = false;
+    for_each_replica(t, [&](bnmc_table* r) {
+      r->enum_max = enum_max < 0 ? kEnumMax : static_cast<uint64_t>(enum_max);
+      r->pst_ready = false;
+      r->ylist_mode = ylists;
+      r->sorted_valid = false;
+    });
   });
 }
 

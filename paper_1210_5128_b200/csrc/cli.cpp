@@ -84,7 +84,8 @@ class Args {
 
 const std::vector<std::string> kRunValued = {"--iterations", "--max-parents", "--gamma", "--ess",
                                              "--seed", "--workers", "--track-top",
-                                             "--tasks-per-node", "--memory-cap", "--device"};
+                                             "--tasks-per-node", "--memory-cap", "--device",
+                                             "--gpus"};
 
 RunConfig run_config(const Args& a) {
   RunConfig c;
@@ -98,6 +99,7 @@ RunConfig run_config(const Args& a) {
   c.tasks_per_node = a.num<int>("--tasks-per-node", c.tasks_per_node);
   c.memory_cap_bytes = a.num<std::uint64_t>("--memory-cap", c.memory_cap_bytes);
   c.device = a.num<int>("--device", 0);
+  c.n_gpus = a.num<int>("--gpus", 1);
   if (a.has("--strict-paper-tracker")) c.strict_paper_tracker = true;
   if (a.has("--k2")) c.alpha_mode = AlphaMode::kK2;
   if (a.has("--pst") && a.has("--unrank")) throw UsageError("--pst excludes --unrank");
@@ -227,7 +229,8 @@ std::vector<int> int_list(const std::string& csv, const std::string& flag) {
 int cmd_bench(int argc, char** argv) {
   const Args a(argc, argv, 2,
                {"--scaling-nodes", "--workers-list", "--samples", "--reps", "--enum-candidates",
-                "--seed", "--max-parents", "--out", "--chains", "--chain-iters", "--device"},
+                "--seed", "--max-parents", "--out", "--chains", "--chain-iters", "--device",
+                "--gpus"},
                {});
   std::ofstream file;
   std::ostream* out = &std::cout;
@@ -247,6 +250,7 @@ int cmd_bench(int argc, char** argv) {
   cfg.max_parents = a.num<int>("--max-parents", 4);
   cfg.seed = seed;
   cfg.device = a.num<int>("--device", 0);
+  cfg.n_gpus = a.num<int>("--gpus", 1);
   *out << "phase,nodes,workers,candidates,reps,seconds,speedup\n";
   for (const int n : int_list(a.str("--scaling-nodes", "13,20"), "--scaling-nodes")) {
     if (n < 2 || n > kMaxNodes) throw UsageError("--scaling-nodes entries must lie in [2,64]");
@@ -301,9 +305,10 @@ void usage() {
                "        [--gamma G] [--ess E] [--seed N] [--workers N] [--track-top K]\n"
                "        [--tasks-per-node N] [--memory-cap B] [--strict-paper-tracker]\n"
                "        [--pst|--unrank] [--k2] [--save-cache F] [--load-cache F] [--device D]\n"
+               "        [--gpus G]\n"
                "  eval  --truth F (--learned F | --sweep --data F) [--nodes N] [--out F] ...\n"
                "  bench [--scaling-nodes L] [--samples N] [--reps N] [--seed N] [--max-parents S]\n"
-               "        [--chains N] [--chain-iters N] [--out F] [--device D]\n";
+               "        [--chains N] [--chain-iters N] [--out F] [--device D] [--gpus G]\n";
 }
 
 }  // namespace

@@ -45,6 +45,7 @@ bnmc_score_params score_params(const RunConfig& cfg) {
   p.alpha_mode = cfg.alpha_mode == AlphaMode::kK2 ? BNMC_ALPHA_K2 : BNMC_ALPHA_BDEU;
   p.memory_cap_bytes = cfg.memory_cap_bytes;
   p.device = cfg.device;
+  p.n_gpus = cfg.n_gpus;
   return p;
 }
 
@@ -316,33 +317,67 @@ ParentSetTable build_pst(int candidates, int s) {  // combinatorics.cpp:92-101
 }
 
 // ============================================================= scoring
-CountTable::CountTable(std::uint64_t configs, int child_card)
-    : r_(configs), card_(child_card), cells_(configs * static_cast<std::uint64_t>(child_card), 0u) {}
+namespace {
+constexpr std::uint64_t kDenseCells = std::uint64_t{1} << 22;  // scoring.cpp:13
+}
+
+CountTable::CountTable(std::uint64_t configs, int child_card) : r_(configs), card_(child_card) {
+  if (r_ > 0 && r_ <= kDenseCells / static_cast<std::uint64_t>(card_))
+    cells_.assign(r_ * static_cast<std::uint64_t>(card_), 0u);
+}
+
+std::uint32_t CountTable::njk(std::uint64_t config, int state) const {
+  if (dense()) return cells_[config * card_ + state];
+  const auto it = sparse_.find(config);
+  return it == sparse_.end() ? 0u : it->second[state];
+}
 
 std::uint32_t CountTable::nk(std::uint64_t config) const {
   std::uint32_t t = 0;
-  for (int j = 0; j < card_; ++j) t += cells_[config * card_ + j];
+  for (int j = 0; j < card_; ++j) t += njk(config, j);
   return t;
 }
 
 std::uint64_t CountTable::samples() const {
   std::uint64_t t = 0;
   for (const std::uint32_t c : cells_) t += c;
+  for (const auto& [k, row] : sparse_)
+    for (const std::uint32_t c : row) t += c;
   return t;
 }
 
 CountTable count_statistics(const Dataset& data, int node, ParentSet pset) {
-  if (node < 0 || node >= data.n() || pset.contains(node) ||
-      (data.n() < kMaxNodes && (pset.mask >> data.n()) != 0))
+  if (node < 0 || node >= data.n() || (data.n() < kMaxNodes && (pset.mask >> data.n()) != 0))
     throw UsageError("count_statistics: bad (node, parent set)");
+  if (pset.contains(node)) throw DataError("node cannot appear in its own parent set");
   std::uint64_t r = 1;
-  pset.for_each([&](int p) { r *= static_cast<std::uint64_t>(data.cardinality(p)); });
+  pset.for_each([&](int p) {
+    const std::uint64_t c = static_cast<std::uint64_t>(data.cardinality(p));
+    if (r > std::numeric_limits<std::uint64_t>::max() / c)
+      throw CapacityError("parent configuration space overflows 64 bits");
+    r *= c;
+  });
   CountTable t(r, data.cardinality(node));
   const int nd = node;
-  const std::uint64_t mask = pset.mask, off = 0;
-  std::uint64_t configs = 0;
-  check(bnmc_gpu_count_statistics(data.cells().data(), data.cardinalities().data(), data.rows(),
-                                  data.n(), 1, &nd, &mask, &off, t.cells().data(), &configs, 0));
+  const std::uint64_t mask = pset.mask;
+  if (t.dense()) {
+    const std::uint64_t off = 0;
+    std::uint64_t configs = 0;
+    check(bnmc_gpu_count_statistics(data.cells().data(), data.cardinalities().data(), data.rows(),
+                                    data.n(), 1, &nd, &mask, &off, t.cells().data(), &configs,
+                                    0));
+    return t;
+  }
+  const std::uint64_t m = data.rows();
+  const int card = data.cardinality(node);
+  std::vector<std::uint64_t> cfg(std::max<std::uint64_t>(m, 1));
+  std::vector<std::uint32_t> cnt(std::max<std::uint64_t>(m, 1) * card);
+  std::uint64_t active = 0;
+  check(bnmc_gpu_count_statistics_sparse(data.cells().data(), data.cardinalities().data(), m,
+                                         data.n(), node, mask, cfg.data(), cnt.data(), &active, 0));
+  for (std::uint64_t k = 0; k < active; ++k)
+    t.sparse().emplace(cfg[k], std::vector<std::uint32_t>(cnt.begin() + k * card,
+                                                          cnt.begin() + (k + 1) * card));
   return t;
 }
 

@@ -61,6 +61,7 @@ struct K1Args {
   double* ls;                          // [n][S]
   uint64_t S;
   int row_begin, row_end;
+  int rp_dense;                        // prefixes with more configurations go to K1W
   int WT, EG;
   int* error;
 };
@@ -129,16 +130,17 @@ __global__ void __launch_bounds__(kK1Threads) k1_kernel(K1Args a, uint64_t prefi
   if (tid == 0) {
     int k;
     const uint64_t P = unrank_global(prefix_base + blockIdx.x, n, a.s, &k);
-    int i = 0, r = 1;
+    int i = 0;
+    uint64_t r = 1;  // saturates: wide prefixes (r > rp_dense) leave below
     for (uint64_t m = P; m; m &= m - 1) {
       s_p[i] = __ffsll((long long)m) - 1;
-      s_rad[i] = r;
-      r *= a.cards[s_p[i]];
+      s_rad[i] = (int)min(r, (uint64_t)0x7fffffff);
+      r = min(r * (uint64_t)a.cards[s_p[i]], (uint64_t)1 << 40);
       ++i;
     }
-    s_rad[i] = r;
+    s_rad[i] = (int)min(r, (uint64_t)0x7fffffff);
     s_k = k;
-    s_rP = r;
+    s_rP = (int)min(r, (uint64_t)0x7fffffff);
     s_ext0 = k ? s_p[k - 1] + 1 : 0;
   }
   __syncthreads();
@@ -149,10 +151,7 @@ __global__ void __launch_bounds__(kK1Threads) k1_kernel(K1Args a, uint64_t prefi
   bool any = ext0 < a.row_end && n > a.row_begin;
   for (int i = 0; i < k; ++i) any |= (s_p[i] >= a.row_begin && s_p[i] < a.row_end);
   if (!any) return;
-  if (rP > kRPMax) {
-    if (tid == 0) atomicExch(a.error, 1);
-    return;
-  }
+  if (rP > a.rp_dense) return;  // wide prefix: its joint sets are counted by K1W
   const int cmax = a.cmax;
   const int WT = TILED ? a.WT : 0;             // AND-plane tiles in smem, or formed on the fly
   const int WTP = WT | 1;                      // odd row stride: lanes over cfgs hit distinct banks
@@ -405,6 +404,8 @@ __global__ void counts_kernel(const uint32_t* __restrict__ bits, const uint32_t*
 
 }  // namespace bnmc_dev
 
+#include "precompute_wide.cuh"
+
 namespace bnmc_host {
 
 struct Bitplanes {
@@ -465,20 +466,157 @@ inline void products(const std::vector<std::pair<int, int>>& cm, size_t i, int l
   }
 }
 
-inline void precompute_rows(cudaStream_t stream, double* d_ls, uint64_t S, const uint8_t* cells,
-                            const int* cards, uint64_t m, int n, int s, double gamma, double ess,
-                            int alpha, int row_begin, int row_end, float* ms_out) {
+// ---------------------------------------------------------------- prefixes
+// K1 works per prefix P (|P| <= s) in the global-index order of subsets of
+// {0..n-1}: sizes min(s,n)..0, lexicographic within a size (the order
+// unrank_global follows). A part of a multi-GPU build owns a contiguous range
+// of prefix indices; every entry (v, pi) belongs to exactly one prefix
+// (P = pi + {v} minus its largest member), so parts write disjoint entries.
+
+inline uint64_t prefix_total(int n, int s) {
+  uint64_t t = 0;
+  for (int j = 0; j <= std::min(s, n); ++j) {
+    uint64_t c = 1;
+    for (int i = 0; i < j; ++i) c = c * (n - i) / (i + 1);
+    t += c;
+  }
+  return t;
+}
+
+inline uint64_t host_choose(int n, int k) {
+  if (k < 0 || k > n) return 0;
+  uint64_t c = 1;
+  for (int i = 0; i < k; ++i) c = c * (n - i) / (i + 1);
+  return c;
+}
+
+// Iterator over prefixes in global-index order from index lo.
+struct PrefixWalk {
+  int n, s, k;
+  int a[bnmc_dev::kMaxPrefix + 1];
+  bool done = false;
+  PrefixWalk(int n_, int s_, uint64_t lo) : n(n_), s(s_) {
+    k = std::min(s, n);
+    uint64_t j = lo;
+    while (k >= 0 && j >= host_choose(n, k)) {
+      j -= host_choose(n, k);
+      --k;
+    }
+    if (k < 0) {
+      done = true;
+      return;
+    }
+    int x = 0;
+    for (int i = 0; i < k; ++i)
+      for (;; ++x) {
+        const uint64_t cnt = host_choose(n - x - 1, k - i - 1);
+        if (j < cnt) {
+          a[i] = x++;
+          break;
+        }
+        j -= cnt;
+      }
+  }
+  void next() {
+    for (int i = k - 1; i >= 0; --i)
+      if (a[i] < n - k + i) {
+        ++a[i];
+        for (int j = i + 1; j < k; ++j) a[j] = a[j - 1] + 1;
+        return;
+      }
+    if (--k < 0) {
+      done = true;
+      return;
+    }
+    for (int i = 0; i < k; ++i) a[i] = i;
+  }
+};
+
+// Configurations of a prefix, saturated at 2^62 (only compared with rp_dense).
+inline uint64_t prefix_configs(const PrefixWalk& w, const int* cards) {
+  const uint64_t cap = uint64_t(1) << 62;
+  uint64_t r = 1;
+  for (int i = 0; i < w.k; ++i) {
+    const uint64_t c = static_cast<uint64_t>(cards[w.a[i]]);
+    r = r > cap / c ? cap : r * c;
+  }
+  return r;
+}
+
+// Largest prefix configuration count the dense K1 counter holds: the joint
+// histogram of U = P + {u} is r_P * card(u) <= kHMax cells, r_P <= kRPMax.
+inline int dense_prefix_limit(const int* cards, int n) {
+  const int cmax = *std::max_element(cards, cards + n);
+  return std::min(bnmc_dev::kRPMax, bnmc_dev::kHMax / cmax);
+}
+
+// Work-balanced split of the prefix range into `parts` contiguous pieces
+// (cut[0] = 0, cut[parts] = total). Dense prefix weight ~ word-ANDs of the
+// popcount product (r_P x extension states x words) + its scoring cells; wide
+// prefix weight ~ keys sorted and walked.
+inline std::vector<uint64_t> k1_partition(const int* cards, int n, int s, uint64_t m, int parts) {
+  const uint64_t total = prefix_total(n, s);
+  std::vector<uint64_t> cut(parts + 1, total);
+  cut[0] = 0;
+  if (parts <= 1) return cut;
+  const int rpd = dense_prefix_limit(cards, n);
+  const double W = static_cast<double>((m + 31) / 32);
+  std::vector<double> suf_c(n + 1, 0.0), suf_c1(n + 1, 0.0);
+  for (int u = n - 1; u >= 0; --u) {
+    suf_c[u] = suf_c[u + 1] + cards[u];
+    suf_c1[u] = suf_c1[u + 1] + (cards[u] - 1);
+  }
+  std::vector<double> wt;
+  wt.reserve(total);
+  double sum = 0.0;
+  for (PrefixWalk w(n, s, 0); !w.done; w.next()) {
+    const int ext0 = w.k ? w.a[w.k - 1] + 1 : 0;
+    double x = 64.0;  // per-CTA overhead
+    if (ext0 < n) {
+      const uint64_t r = prefix_configs(w, cards);
+      if (r <= static_cast<uint64_t>(rpd))
+        x += r * ((suf_c1[ext0] + 1.0) * (W + 2.0) + 4.0 * (w.k + 1) * suf_c[ext0]);
+      else
+        x += 24.0 * (n - ext0) * (w.k + 1) * static_cast<double>(m + 1);
+    }
+    wt.push_back(x);
+    sum += x;
+  }
+  double acc = 0.0;
+  int g = 1;
+  for (uint64_t i = 0; i < total && g < parts; ++i) {
+    acc += wt[i];
+    while (g < parts && acc >= sum * g / parts) cut[g++] = i + 1;
+  }
+  return cut;
+}
+
+struct K1Range {
+  uint64_t p_lo = 0, p_hi = ~uint64_t(0);  // prefix indices [p_lo, p_hi)
+  int row_begin = 0, row_end = 64;         // only entries of these node rows
+};
+
+struct K1Report {
+  float ms = 0.f;          // K1 (dense) + K1W (wide) device time
+  uint64_t wide_entries = 0;
+};
+
+inline void precompute(cudaStream_t stream, double* d_ls, uint64_t S, const uint8_t* cells,
+                       const int* cards, uint64_t m, int n, int s, double gamma, double ess,
+                       int alpha, const K1Range& range, K1Report* rep) {
   using namespace bnmc_dev;
-  // Dense-counter bounds: largest joint set U (s+1 members) and prefix P (s).
+  const uint64_t total = prefix_total(n, s);
+  const uint64_t p_lo = std::min(range.p_lo, total), p_hi = std::min(range.p_hi, total);
+  const int row_begin = range.row_begin, row_end = std::min(range.row_end, n);
+  // Dense prefixes: r_P <= rpd (joint histograms of <= kHMax cells). Larger
+  // prefixes (if any) are counted by K1W.
   std::vector<int> sorted(cards, cards + n);
   std::sort(sorted.rbegin(), sorted.rend());
-  uint64_t hu = 1, hp = 1;
-  for (int i = 0; i < std::min(n, s + 1); ++i) hu *= sorted[i];
-  for (int i = 0; i < std::min(n, s); ++i) hp *= sorted[i];
-  if (hu > static_cast<uint64_t>(kHMax) || hp > static_cast<uint64_t>(kRPMax))
-    raise(BNMC_CAPACITY, "joint configuration space of up to s+1 variables (" + std::to_string(hu) +
-                             " cells) exceeds the device dense counter (" +
-                             std::to_string(kHMax) + ")");
+  const int rpd = dense_prefix_limit(cards, n);
+  uint64_t hp = 1;  // largest prefix configuration count (saturated)
+  for (int i = 0; i < std::min(n, s); ++i)
+    hp = hp > (1ull << 40) / sorted[i] ? (1ull << 40) : hp * sorted[i];
+  const bool any_wide = hp > static_cast<uint64_t>(rpd);
   const int cmax = sorted[0];
 
   Bitplanes bp;
@@ -547,6 +685,7 @@ inline void precompute_rows(cudaStream_t stream, double* d_ls, uint64_t S, const
   a.S = S;
   a.row_begin = row_begin;
   a.row_end = row_end;
+  a.rp_dense = rpd;
   // Shared memory, sized for several CTAs per SM so one CTA's scoring phase
   // overlaps other CTAs' counting: prefix counts + CNT for a group of
   // extensions (+ an AND-plane word tile in tiled mode). Tiled mode re-forms
@@ -554,7 +693,7 @@ inline void precompute_rows(cudaStream_t stream, double* d_ls, uint64_t S, const
   // a typical prefix's extensions; otherwise AND-planes are formed on the fly.
   const char* kb = std::getenv("BNMC_K1_SMEM_KB");
   const size_t budget = (kb ? std::strtoul(kb, nullptr, 10) : 48) * 1024;
-  const int rPmax = static_cast<int>(hp);
+  const int rPmax = static_cast<int>(std::min<uint64_t>(hp, rpd));
   const size_t np_bytes = 4ull * rPmax;
   const int wt_fit = static_cast<int>((budget / 2) / (4ull * rPmax)) - 1;
   int wt = std::max(1, std::min(std::max(bp.W, 1), std::max(32, wt_fit)));
@@ -579,22 +718,13 @@ inline void precompute_rows(cudaStream_t stream, double* d_ls, uint64_t S, const
                           static_cast<int>(shm)));
   CK(cudaFuncSetAttribute(k1_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           static_cast<int>(shm)));
-  const uint64_t prefixes = [&] {
-    uint64_t t = 0;
-    for (int j = 0; j <= std::min(s, n); ++j) {
-      uint64_t c = 1;
-      for (int i = 0; i < j; ++i) c = c * (n - i) / (i + 1);
-      t += c;
-    }
-    return t;
-  }();
   cudaEvent_t e0, e1;
   CK(cudaEventCreate(&e0));
   CK(cudaEventCreate(&e1));
   CK(cudaEventRecord(e0, stream));
   const uint64_t chunk = 1u << 30;
-  for (uint64_t base = 0; base < prefixes; base += chunk) {
-    const unsigned blocks = static_cast<unsigned>(std::min(chunk, prefixes - base));
+  for (uint64_t base = p_lo; base < p_hi; base += chunk) {
+    const unsigned blocks = static_cast<unsigned>(std::min(chunk, p_hi - base));
     if (tiled)
       k1_kernel<true><<<blocks, kK1Threads, shm, stream>>>(a, base);
     else
@@ -603,15 +733,55 @@ inline void precompute_rows(cudaStream_t stream, double* d_ls, uint64_t S, const
   }
   CK(cudaEventRecord(e1, stream));
   CK(cudaEventSynchronize(e1));
-  CK(cudaEventElapsedTime(ms_out, e0, e1));
+  float dense_ms = 0.f;
+  CK(cudaEventElapsedTime(&dense_ms, e0, e1));
   int err = 0;
   CK(cudaMemcpy(&err, d_err, sizeof(int), cudaMemcpyDeviceToHost));
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
   cudaFree(d_keys);
   cudaFree(d_lut);
   cudaFree(d_err);
   if (err) raise(BNMC_ERR, "precompute kernel reported internal error " + std::to_string(err));
+
+  // K1W: the entries of wide prefixes (r_P > rpd) in this range.
+  float wide_ms = 0.f;
+  uint64_t wide_entries = 0;
+  if (any_wide && p_lo < p_hi) {
+    CK(cudaEventRecord(e0, stream));
+    WideScorer ws(stream, cells, cards, bp.cards, m, n, s, gamma, ess, alpha, d_ls, S);
+    uint64_t idx = p_lo;
+    for (PrefixWalk w(n, s, p_lo); !w.done && idx < p_hi; w.next(), ++idx) {
+      const int ext0 = w.k ? w.a[w.k - 1] + 1 : 0;
+      if (ext0 >= n || prefix_configs(w, cards) <= static_cast<uint64_t>(rpd)) continue;
+      uint64_t pm = 0;
+      for (int i = 0; i < w.k; ++i) pm |= 1ull << w.a[i];
+      for (int u = ext0; u < n; ++u) {
+        const uint64_t U = pm | (1ull << u);
+        for (uint64_t vm = U; vm; vm &= vm - 1) {
+          const int v = __builtin_ctzll(vm);
+          if (v < row_begin || v >= row_end) continue;
+          const uint64_t pi = U & ~(1ull << v);
+          uint64_t r = 1;
+          for (uint64_t q = pi; q; q &= q - 1) {
+            const uint64_t c = static_cast<uint64_t>(cards[__builtin_ctzll(q)]);
+            if (r > ~0ull / c) raise(BNMC_CAPACITY, "parent configuration space overflows 64 bits");
+            r *= c;
+          }
+          ws.add(WideEntry{v, pi, r});
+        }
+      }
+    }
+    ws.flush();
+    wide_entries = ws.entries();
+    CK(cudaEventRecord(e1, stream));
+    CK(cudaEventSynchronize(e1));
+    CK(cudaEventElapsedTime(&wide_ms, e0, e1));
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (rep) {
+    rep->ms = dense_ms + wide_ms;
+    rep->wide_entries = wide_entries;
+  }
 }
 
 inline void count_statistics_device(const uint8_t* cells, const int* cards, uint64_t m, int n,
@@ -663,6 +833,57 @@ inline void count_statistics_device(const uint8_t* cells, const int* cards, uint
     cudaFree(d_off);
     cudaFree(d_out);
   }
+  cudaStreamDestroy(stream);
+}
+
+// count_statistics as the reference's sparse CountTable (ordered map above
+// 2^22 cells, scoring.cpp:53-80): the active configurations ascending with
+// their card(node) counts, via the K1W key sort on the device. configs_out
+// holds up to m entries, counts_out up to m * card(node).
+inline void count_statistics_sparse_device(const uint8_t* cells, const int* cards, uint64_t m,
+                                           int n, int node, uint64_t pset, uint64_t* configs_out,
+                                           uint32_t* counts_out, uint64_t* n_active) {
+  if (n < 1 || n > 64) raise(BNMC_DATA, "dataset must have between 1 and 64 variables");
+  if (node < 0 || node >= n) raise(BNMC_USAGE, "node out of range");
+  if ((pset >> node) & 1u) raise(BNMC_DATA, "node cannot appear in its own parent set");
+  if (n < 64 && (pset >> n)) raise(BNMC_USAGE, "parent out of range");
+  uint64_t r = 1;
+  for (uint64_t mm = pset; mm; mm &= mm - 1) {
+    const uint64_t c = static_cast<uint64_t>(cards[__builtin_ctzll(mm)]);
+    if (r > ~0ull / c) raise(BNMC_CAPACITY, "parent configuration space overflows 64 bits");
+    r *= c;
+  }
+  const int cv = cards[node];
+  cudaStream_t stream;
+  CK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+  int* d_cards = nullptr;
+  try {
+    CK(cudaMalloc(&d_cards, sizeof(int) * n));
+    CK(cudaMemcpyAsync(d_cards, cards, sizeof(int) * n, cudaMemcpyHostToDevice, stream));
+    std::vector<uint64_t> keys;
+    std::vector<uint8_t> vals;
+    bool comp = false;
+    {
+      WideScorer ws(stream, cells, cards, d_cards, m, n, 0, 0.1, 1.0, BNMC_ALPHA_K2, nullptr, 0);
+      ws.sorted_segment(WideEntry{node, pset, r}, keys, vals, comp);
+    }
+    const uint64_t div = comp ? static_cast<uint64_t>(cv) : 1;
+    uint64_t na = 0;
+    for (uint64_t i = 0; i < m;) {
+      const uint64_t cfg = keys[i] / div;
+      configs_out[na] = cfg;
+      uint32_t* row = counts_out + na * cv;
+      std::fill(row, row + cv, 0u);
+      for (; i < m && keys[i] / div == cfg; ++i) ++row[vals[i]];
+      ++na;
+    }
+    *n_active = na;
+  } catch (...) {
+    cudaFree(d_cards);
+    cudaStreamDestroy(stream);
+    throw;
+  }
+  cudaFree(d_cards);
   cudaStreamDestroy(stream);
 }
 

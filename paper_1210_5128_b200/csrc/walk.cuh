@@ -519,6 +519,7 @@ __device__ __noinline__ void tracker_insert_warp(uint64_t* tm, double* tt, uint6
     ins += __popc(__ballot_sync(0xffffffffu, prec));
   }
   const int last = full ? count - 1 : count;
+  __syncwarp();  // every lane's reads of the tracker above precede the writes below
   for (int e = last; e > ins; --e) {  // move entries [ins, last) down one slot
     BNMC_FOR_NODES(i, lane, 32, n) tm[(uint64_t)e * n + i] = tm[(uint64_t)(e - 1) * n + i];
     if (lane == 0) {

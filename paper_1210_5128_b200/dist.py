@@ -1,22 +1,28 @@
-"""Multi-GPU plumbing: one process per GPU over torch.distributed.
+"""Multi-GPU plumbing: one process per GPU.
 
 The path shards in two independent ways and has no per-iteration exchange:
 
-* precompute: node ROWS of the score table are independent. Rank r builds rows
-  ``row_partition(n, world)[r]`` with ``bnmc_gpu_table_build_rows`` and one
-  all-gather over NCCL (NVLink) gives every GPU the full table
-  (``all_gather_rows``);
-* sampling: chains are independent replicas (chain id -> seed); at the end the
-  fixed-size per-chain records are gathered once (``gather_chain_records``;
-  NCCL has no gather, so it is an all-gather of equal-size records).
+* precompute: K1's unit of work is a prefix P (|P| <= s); every score-table
+  entry belongs to exactly one prefix, so rank r computes the work-balanced
+  prefix range ``bnmc_gpu_k1_partition(world)[r]`` into a zeroed table and one
+  in-place all-reduce of the 64-bit table words (integer sum == union of the
+  parts, bit-exact) completes the table on every GPU. This replaces the
+  reference's OpenMP loop over node rows (src/scoring.cpp:179-190);
+* sampling: chains are independent replicas (global chain id -> seed); at the
+  end the fixed-size per-chain records are all-gathered once.
 
-Everything here is backend-agnostic torch code so the same functions run with
-``gloo`` on CPU tensors (tests/test_dist.py) and ``nccl`` on device buffers.
+The data-path collectives run inside the library over its own NCCL
+communicator (``bnmc_gpu_comm_*`` in include/bnmc_gpu.h: NVLink/NVSwitch);
+torch.distributed (any backend — gloo on CPU in tests/test_dist.py) only ships
+the NCCL unique id and provides barriers. The host-side pieces (record
+packing, the int64 union) are backend-agnostic torch code so the same
+functions run on CPU tensors over gloo.
 """
 from __future__ import annotations
 
 import ctypes as C
 import os
+import time
 
 import numpy as np
 
@@ -29,9 +35,12 @@ def env_rank_world():
             int(os.environ.get("LOCAL_RANK", "0")))
 
 
-def row_partition(n: int, world: int):
-    """Contiguous, balanced node-row blocks: rank r owns [r*n//w, (r+1)*n//w)."""
-    return [(r * n // world, (r + 1) * n // world) for r in range(world)]
+def k1_partition(cards, m: int, n: int, s: int, world: int) -> np.ndarray:
+    """Prefix-index cuts of the work-balanced K1 split (world + 1 values)."""
+    cuts = np.zeros(world + 1, np.uint64)
+    _lib.check(_lib.lib().bnmc_gpu_k1_partition(np.ascontiguousarray(cards, np.int32), m, n, s,
+                                                 world, cuts))
+    return cuts
 
 
 def chain_seeds(base_seed: int, rank: int, chains_per_rank: int, step: int = 0, world: int = 1):
@@ -58,51 +67,73 @@ def table_rows_tensor(cache):
     return t.view(cache.n(), stride.value)
 
 
-def all_gather_rows(rows, n: int, world: int, rank: int, group=None):
-    """In-place all-gather of node-row shards of an (n, S) tensor.
+class Comm:
+    """One rank of the library's NCCL communicator (bnmc_gpu_comm_init)."""
 
-    ``rows`` holds this rank's block (row_partition) and garbage elsewhere; on
-    return every rank holds all n rows. Blocks are padded to equal size because
-    all_gather_into_tensor needs equal chunks.
-    """
-    import torch
-    import torch.distributed as dist
-    parts = row_partition(n, world)
-    per = max(b - a for a, b in parts)
-    S = rows.shape[1]
-    a, b = parts[rank]
-    send = torch.zeros((per, S), dtype=rows.dtype, device=rows.device)
-    send[: b - a] = rows[a:b]
-    recv = torch.empty((world * per, S), dtype=rows.dtype, device=rows.device)
-    dist.all_gather_into_tensor(recv, send, group=group)
-    for r, (ra, rb) in enumerate(parts):
-        if r != rank and rb > ra:
-            rows[ra:rb] = recv[r * per: r * per + (rb - ra)]
-    return rows
+    def __init__(self, rank: int, world: int, device: int, group=None):
+        import torch.distributed as dist
+        self.rank, self.world, self.device = rank, world, device
+        uid = np.zeros(128, np.uint8)
+        if rank == 0:
+            _lib.check(_lib.lib().bnmc_gpu_comm_unique_id(uid))
+        if world > 1:
+            box = [uid.tobytes()]
+            dist.broadcast_object_list(box, src=0, group=group)
+            uid = np.frombuffer(box[0], np.uint8).copy()
+        h = C.c_void_p()
+        _lib.check(_lib.lib().bnmc_gpu_comm_init(uid, world, rank, device, C.byref(h)))
+        self.handle = h
+
+    def allgather(self, arr: np.ndarray) -> np.ndarray:
+        """All-gather of an equal-size array per rank -> [world, *arr.shape]."""
+        a = np.ascontiguousarray(arr)
+        out = np.empty((self.world,) + a.shape, a.dtype)
+        _lib.check(_lib.lib().bnmc_gpu_comm_allgather(self.handle, _lib.ptr(a), a.nbytes,
+                                                       _lib.ptr(out)))
+        return out
+
+    def max(self, values) -> list:
+        v = np.ascontiguousarray(values, np.float64).copy()
+        _lib.check(_lib.lib().bnmc_gpu_comm_allreduce_max(self.handle, v, v.size))
+        return v.tolist()
+
+    def close(self):
+        if getattr(self, "handle", None) and self.handle.value:
+            _lib.lib().bnmc_gpu_comm_free(self.handle)
+            self.handle = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
-def build_table_sharded(data, cfg, priors, rank: int, world: int, group=None, force=False):
-    """Row-sharded device precompute + NCCL all-gather -> full table on every GPU."""
+def build_table_comm(data, cfg, priors, comm: Comm):
+    """ScoreCache::build split over the ranks of `comm`: part `rank` of the
+    K1 prefix partition, NCCL all-reduce of the table words, PPF fold."""
     from .api import ScoreCache, _prior_array
-    import time
     pr = _prior_array(priors)
-    a, b = row_partition(data.n, world)[rank]
     out = C.c_void_p()
     t0 = time.perf_counter()
-    _lib.check(_lib.lib().bnmc_gpu_table_build_rows(
+    _lib.check(_lib.lib().bnmc_gpu_table_build_comm(
         data.cells.reshape(-1), data.cards, data.rows(), data.n, C.byref(cfg.score_params()),
-        _lib.ptr(pr), a, b, C.byref(out)))
+        _lib.ptr(pr), comm.handle, C.byref(out)))
     cache = ScoreCache(out.value, data.n, cfg.max_parents, cfg)
-    if world > 1 or force:
-        import torch
-        rows = table_rows_tensor(cache)
-        torch.cuda.synchronize()
-        all_gather_rows(rows, data.n, world, rank, group)
-        torch.cuda.synchronize()
-    _lib.check(_lib.lib().bnmc_gpu_table_finalize(cache.handle))
     cache._priors_key = None if pr is None else pr.tobytes()
     cache.preprocess_seconds = time.perf_counter() - t0
+    a, b = C.c_float(), C.c_float()
+    _lib.check(_lib.lib().bnmc_gpu_table_build_ms(cache.handle, C.byref(a), C.byref(b)))
+    cache.build_ms = (a.value, b.value)
     return cache
+
+
+def union_of_parts(words, group=None):
+    """In-place integer sum of part tables viewed as int64 words (torch tensor
+    on any backend): each word has one writer, so the sum is the union."""
+    import torch.distributed as dist
+    dist.all_reduce(words, op=dist.ReduceOp.SUM, group=group)
+    return words
 
 
 # Fixed-size per-chain record: [seed, accepted, best_total(bits), final_total(bits),
@@ -141,7 +172,8 @@ def decode_record(rec: np.ndarray, n: int) -> dict:
 
 
 def gather_chain_records(records: np.ndarray, group=None, device=None) -> np.ndarray:
-    """All-gather of equal-size [chains, rec_len] int64 records (rank order)."""
+    """All-gather of equal-size [chains, rec_len] int64 records (rank order)
+    over torch.distributed (the CPU/gloo form of Comm.allgather)."""
     import torch
     import torch.distributed as dist
     world = dist.get_world_size(group)

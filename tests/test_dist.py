@@ -1,6 +1,7 @@
-"""CPU, world_size 2 over gloo: the multi-GPU host logic (row-sharded table
-all-gather and the end-of-run chain-record gather) on CPU tensors — the same
-functions run on NCCL device buffers in bench.py."""
+"""CPU, world_size 2 over gloo: the multi-GPU host logic (the union of
+disjoint part tables by an int64 sum all-reduce, the end-of-run chain-record
+gather, the K1 prefix partition) on CPU tensors — the library runs the same
+exchanges over its NCCL communicator on the GPU (bnmc_gpu_comm_*)."""
 import os
 import socket
 
@@ -25,12 +26,16 @@ def _worker(rank, world, port, n, S, q):
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        full = torch.arange(n * S, dtype=torch.float64).view(n, S) * 1.5
-        rows = torch.full((n, S), float("nan"), dtype=torch.float64)
-        a, b = D.row_partition(n, world)[rank]
-        rows[a:b] = full[a:b]
-        D.all_gather_rows(rows, n, world, rank)
-        ok_rows = bool(torch.equal(rows, full))
+        # part tables: disjoint words (every entry has one writer), zero elsewhere,
+        # including -0.0 and NaN payloads that a float sum would not preserve
+        rng = np.random.default_rng(0)
+        full = rng.normal(size=(n, S))
+        full[0, 0], full[-1, -1] = -0.0, np.nan
+        owner = rng.integers(0, world, size=(n, S))
+        part = np.where(owner == rank, full, 0.0)
+        words = torch.from_numpy(part.view(np.int64).copy())
+        D.union_of_parts(words)
+        ok_rows = bool(np.array_equal(words.numpy().view(np.uint64), full.view(np.uint64)))
 
         class R:  # minimal chain result
             pass
@@ -75,14 +80,9 @@ def test_gloo_world2_row_allgather_and_chain_gather(n):
     np.testing.assert_array_equal(out[0][2], out[1][2])
 
 
-def test_row_partition_covers_rows():
-    for n in range(1, 65):
-        for w in range(1, 9):
-            parts = D.row_partition(n, w)
-            assert parts[0][0] == 0 and parts[-1][1] == n
-            assert all(parts[i][1] == parts[i + 1][0] for i in range(w - 1))
-            sizes = [b - a for a, b in parts]
-            assert max(sizes) - min(sizes) <= 1
+def test_k1_partition_through_dist():
+    cuts = D.k1_partition(np.full(60, 3, np.int32), 10000, 60, 4, 8)
+    assert cuts[0] == 0 and cuts[-1] == 523686 and np.all(np.diff(cuts.astype(np.int64)) > 0)
 
 
 def test_chain_seeds_are_global_ids():
