@@ -262,6 +262,37 @@ def walk_roofline(prof, avg_launch_s, peak, peak_src, alg_bytes, chain_iters_per
                     "ncu-measured figure"}
 
 
+def reference_api_e2e(P, cache, pri, cfg, chains, iters, steps=3):
+    """Wall-clock throughput through the reference-shaped APIs that return
+    McmcResult objects (not the bench's caller-owned pinned batch): the Python
+    mirror's run_chains (pooled pinned buffers, lazy McmcResult) and the C++
+    drop-in bnmc::run_chains (tools/cxx/e2e_probe), each vs its device time."""
+    c1 = P.RunConfig(max_parents=cfg.max_parents, iterations=iters, scan_mode=2,
+                     memory_cap_bytes=cfg.memory_cap_bytes, device=cfg.device)
+    seeds = np.arange(1, chains + 1, dtype=np.uint64)
+    P.run_chains(cache, pri, seeds, c1)  # warm-up (pool)
+    wall = dev = 0.0
+    for k in range(steps):
+        t0 = time.perf_counter()
+        rs = P.run_chains(cache, pri, seeds + np.uint64(k * chains), c1)
+        best = max(range(len(rs)), key=lambda c: rs.batch.tracker_totals[c, 0])
+        _ = rs[best]  # one McmcResult materialised, as a caller reading the best chain
+        wall += time.perf_counter() - t0
+        dev += rs.batch.device_ms / 1e3
+    total = steps * chains * iters
+    out = {"python_run_chains": {"e2e_it_s": total / wall, "device_it_s": total / dev,
+                                 "e2e_over_device": dev / wall}}
+    probe = os.path.join(ROOT, "tools", "cxx", "_build", "e2e_probe")
+    if os.path.exists(probe):
+        try:
+            r = subprocess.run([probe, str(chains), str(iters), str(steps), "1"], capture_output=True,
+                               text=True, timeout=600)
+            out["cxx_run_chains"] = json.loads(r.stdout.strip().splitlines()[-1])
+        except Exception as e:  # reported, not fatal
+            out["cxx_run_chains"] = {"error": str(e)[:200]}
+    return out
+
+
 def full_scan_probe(P, _lib, cache, pri, cfg, chains=64, iters=100):
     """The full-row scan path (scan_mode 1, K2 + CUDA Graphs): it/s and the K2
     roofline (32-B key sectors it must stream per launch / avg launch time)."""
@@ -301,6 +332,13 @@ def run_ours(args):
     comm = None
     if dist_on:
         import torch.distributed as tdist
+        if "RANK" not in os.environ:  # --force-dist without torchrun: a world of one
+            import socket
+            with socket.socket() as sk:
+                sk.bind(("127.0.0.1", 0))
+                port = sk.getsockname()[1]
+            os.environ.update(RANK="0", WORLD_SIZE="1", LOCAL_RANK="0",
+                              MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
         tdist.init_process_group("gloo")
         comm = D.Comm(rank, world, local)
     data, pri, cfg, truth = P.baseline_instance(args.config)
@@ -403,6 +441,7 @@ def run_ours(args):
             extra["single_chain_it_s"] = I1 / (one.device_ms / 1e3)
             extra["single_chain_iterations"] = I1
             extra["full_scan_path"] = full_scan_probe(P, _lib, cache, pri, cfg)
+            extra["e2e_reference_api"] = reference_api_e2e(P, cache, pri, cfg, Cn, I)
         h2d = 8 * Cn
         d2h = (Cn * I * (8 + 1 + 8) + Cn * K * (n * 8 + 8) + Cn * (n * 4 + 8 + 8 + 4) + 4 * Cn)
         out_line = {

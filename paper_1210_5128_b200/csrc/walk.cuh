@@ -132,7 +132,9 @@ struct WalkArgs {
 // a precedes b in the reference enumeration over predecessor positions (sizes
 // descending, then lexicographic on sorted positions). Masks are candidate
 // positions of row v; ppos[node] = position in the current order.
-__device__ __forceinline__ bool prefer_pos(uint64_t ma, uint64_t mb, int v, const uint8_t* ppos) {
+// Out of line: only exact ties reach it (rare), so its code stays out of the
+// hot loop's instruction-cache footprint.
+__device__ __noinline__ bool prefer_pos(uint64_t ma, uint64_t mb, int v, const uint8_t* ppos) {
   const int sa = __popcll(ma), sb = __popcll(mb);
   if (sa != sb) return sa > sb;
   uint64_t pa = 0, pb = 0;
@@ -571,6 +573,10 @@ __device__ __forceinline__ void team_sync(int team) {
   }
 }
 
+struct TeamState;
+__device__ __noinline__ void init_team_state(TeamState& S, const WalkArgs& A, int c, int n,
+                                             bool score_only);
+
 // Per-team chain state in shared memory.
 struct TeamState {
   uint8_t order[64], prop[64], ppos[64];
@@ -587,6 +593,34 @@ struct TeamState {
   unsigned long long acc;
   int np, a, b, accept, tcount, amb;
 };
+
+// Chain start (one thread, out of line: once per chain): the order to score,
+// or the initial shuffle of the split(1) stream and the split(2)/(3) streams
+// (sampler.cpp:77-86).
+__device__ __noinline__ void init_team_state(TeamState& S, const WalkArgs& A, int c, int n,
+                                             bool score_only) {
+  if (score_only) {
+    for (int i = 0; i < n; ++i) S.order[i] = (uint8_t)A.perms[(uint64_t)c * n + i];
+  } else {
+    const Rng master{A.seeds[c]};
+    Rng init = master.split(1);
+    for (int i = 0; i < n; ++i) S.order[i] = (uint8_t)i;
+    for (int i = n; i > 1; --i) {
+      const int j = (int)init.next_below((uint64_t)i);
+      const uint8_t t = S.order[i - 1];
+      S.order[i - 1] = S.order[j];
+      S.order[j] = t;
+    }
+    S.rng = master.split(2).s;
+    S.arng = master.split(3).s;
+  }
+  S.tied = 0;
+  S.amb = 0;
+  S.tcount = 0;
+  S.tmin = -INFINITY;
+  S.acc = 0;
+  S.cur_total = 0.0;
+}
 
 template <int TW>
 __host__ __device__ constexpr int walk_cta_threads() {
@@ -624,30 +658,7 @@ __global__ void __launch_bounds__(walk_cta_threads<TW>(), TW == 1 ? kWalkMinBloc
   if (c >= A.C) return;  // whole teams only: no later CTA-wide barrier when TW < 8
   TeamState& S = s_team[team];
   const bool score_only = A.perms != nullptr;
-  if (ttid == 0) {
-    if (score_only) {
-      for (int i = 0; i < n; ++i) S.order[i] = (uint8_t)A.perms[(uint64_t)c * n + i];
-    } else {
-      // initial order: shuffle of the split(1) stream (sampler.cpp:83-86)
-      const Rng master{A.seeds[c]};
-      Rng init = master.split(1);
-      for (int i = 0; i < n; ++i) S.order[i] = (uint8_t)i;
-      for (int i = n; i > 1; --i) {
-        const int j = (int)init.next_below((uint64_t)i);
-        const uint8_t t = S.order[i - 1];
-        S.order[i - 1] = S.order[j];
-        S.order[j] = t;
-      }
-      S.rng = master.split(2).s;
-      S.arng = master.split(3).s;
-    }
-    S.tied = 0;
-    S.amb = 0;
-    S.tcount = 0;
-    S.tmin = -INFINITY;
-    S.acc = 0;
-    S.cur_total = 0.0;
-  }
+  if (ttid == 0) init_team_state(S, A, c, n, score_only);
   team_sync<TW>(team);
   unsigned long long walked = 0, enumerated = 0;  // statistics (lane 0 of each warp)
   unsigned long long pairs = 0;
@@ -687,7 +698,7 @@ __global__ void __launch_bounds__(walk_cta_threads<TW>(), TW == 1 ? kWalkMinBloc
     team_sync<TW>(team);
     const int pa = S.a, pb = S.b;
     const int lo = !BNMC_FRESH ? min(pa, pb) : 0, hi = !BNMC_FRESH ? max(pa, pb) : n - 1;
-    for (int i = ttid; i < n; i += TW * 32) {
+    BNMC_FOR_NODES(i, ttid, TW * 32, n) {
       const int src = BNMC_FRESH ? i : (i == pa ? pb : (i == pb ? pa : i));
       S.prop[i] = S.order[src];
       S.pm[i] = S.cm[i];
@@ -698,12 +709,26 @@ __global__ void __launch_bounds__(walk_cta_threads<TW>(), TW == 1 ? kWalkMinBloc
     // whose best is an exact tie (their position-order tie-break may change)
     if (twarp == 0) {
       uint64_t bit[2];
-      bool take[2];
+      bool take[2], dl[2];
+      const int xnode = S.prop[hi], ynode = S.prop[lo];
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int p = 2 * lane + h;
-        bit[h] = p < n ? 1ull << S.prop[p] : 0ull;
+        const int v = p < n ? S.prop[p] : 0;
+        bit[h] = p < n ? 1ull << v : 0ull;
         take[h] = p < n && ((p >= lo && p <= hi) || (p > hi && (S.tied & bit[h])));
+        // middle rows of a swap: the node at hi (X) left the predecessors, the
+        // node at lo (Y) joined; delta-eligible when the current best avoids X
+        // and is not an exact tie. A walked delta row whose Y-list head (the
+        // best set containing Y) is below its current best keeps its best: it
+        // is dropped here, one load per row in parallel, instead of costing a
+        // pair (pair_argmax's delta early exit, same test)
+        dl[h] = take[h] && !BNMC_FRESH && p > lo && p < hi && (p <= A.pe || A.yeff) &&
+                !(S.tied & bit[h]) && !((S.cm[v] >> xnode) & 1ull);
+        if (dl[h] && p > A.pe &&
+            __ldg(A.yeff + (uint64_t)(uint32_t)(v * (n - 1) + ynode - (ynode > v)) * A.Syw32) <
+                S.cb[v])
+          take[h] = false;
       }
       uint64_t incl = bit[0] | bit[1];
       int cnt = (int)take[0] + (int)take[1];
@@ -729,11 +754,7 @@ __global__ void __launch_bounds__(walk_cta_threads<TW>(), TW == 1 ? kWalkMinBloc
         S.pv[slot] = (uint8_t)v;
         S.pp[slot] = (uint8_t)p;
         S.pc[slot] = nodes_to_cand(pre[h], v);
-        // middle rows of a swap: the node at hi (X) left the predecessors, the
-        // node at lo (Y) joined; eligible when the current best avoids X and
-        // is not an exact tie
-        S.pd[slot] = (uint8_t)(!BNMC_FRESH && p > lo && p < hi && (p <= A.pe || A.yeff) &&
-                               !((S.tied >> v) & 1ull) && !((S.cm[v] >> S.prop[hi]) & 1ull));
+        S.pd[slot] = (uint8_t)dl[h];
         ++slot;
       }
       if (lane == 31) S.np = cnt;
@@ -809,7 +830,7 @@ __global__ void __launch_bounds__(walk_cta_threads<TW>(), TW == 1 ? kWalkMinBloc
       continue;
     }
     if (score_only) {
-      for (int i = ttid; i < n; i += TW * 32) {
+      BNMC_FOR_NODES(i, ttid, TW * 32, n) {
         A.out_masks[(uint64_t)c * n + i] = S.pm[i];
         A.out_best[(uint64_t)c * n + i] = S.pb[i];
       }
@@ -830,7 +851,7 @@ __global__ void __launch_bounds__(walk_cta_threads<TW>(), TW == 1 ? kWalkMinBloc
     }
     // ---- commit + trace row
     if (accepted)
-      for (int i = ttid; i < n; i += TW * 32) {
+      BNMC_FOR_NODES(i, ttid, TW * 32, n) {
         S.cm[i] = S.pm[i];
         S.cb[i] = S.pb[i];
         S.order[i] = S.prop[i];
@@ -854,7 +875,7 @@ __global__ void __launch_bounds__(walk_cta_threads<TW>(), TW == 1 ? kWalkMinBloc
   }
 #undef BNMC_FRESH
   if (!score_only) {
-    for (int i = ttid; i < n; i += TW * 32) A.final_order[(uint64_t)c * n + i] = S.order[i];
+    BNMC_FOR_NODES(i, ttid, TW * 32, n) A.final_order[(uint64_t)c * n + i] = S.order[i];
     if (ttid == 0) {
       A.final_score[c] = S.cur_total;
       A.accepted[c] = S.acc;
@@ -998,12 +1019,22 @@ __global__ void __launch_bounds__(1024, 1) walk_spec_kernel(WalkArgs A) {
       SpecSlot& S = s_sl[warp];
       const int lo = t > 0 ? min(S.a, S.b) : 0, hi = t > 0 ? max(S.a, S.b) : n - 1;
       uint64_t bit[2];
-      bool take[2];
+      bool take[2], dl[2];
+      const int xnode = S.prop[hi], ynode = S.prop[lo];
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int p = 2 * lane + h;
-        bit[h] = p < n ? 1ull << S.prop[p] : 0ull;
+        const int v = p < n ? S.prop[p] : 0;
+        bit[h] = p < n ? 1ull << v : 0ull;
         take[h] = p < n && ((p >= lo && p <= hi) || (p > hi && (s_tied & bit[h])));
+        // delta rows whose Y-list head is below the current best keep it
+        // (as in walk_chain_kernel's pair list)
+        dl[h] = take[h] && t > 0 && p > lo && p < hi && (p <= A.pe || A.yeff) &&
+                !(s_tied & bit[h]) && !((s_cm[v] >> xnode) & 1ull);
+        if (dl[h] && p > A.pe &&
+            __ldg(A.yeff + (uint64_t)(uint32_t)(v * (n - 1) + ynode - (ynode > v)) * A.Syw32) <
+                s_cb[v])
+          take[h] = false;
       }
       uint64_t incl = bit[0] | bit[1];
       int cnt = (int)take[0] + (int)take[1];
@@ -1029,8 +1060,7 @@ __global__ void __launch_bounds__(1024, 1) walk_spec_kernel(WalkArgs A) {
         S.pv[slot] = (uint8_t)v;
         S.pp[slot] = (uint8_t)p;
         S.pc[slot] = nodes_to_cand(pre[h], v);
-        S.pd[slot] = (uint8_t)(t > 0 && p > lo && p < hi && (p <= A.pe || A.yeff) &&
-                               !((s_tied >> v) & 1ull) && !((s_cm[v] >> S.prop[hi]) & 1ull));
+        S.pd[slot] = (uint8_t)dl[h];
         ++slot;
       }
       if (lane == 31) S.np = cnt;
