@@ -186,6 +186,14 @@ struct bnmc_table {
   DevBuf<uint64_t> ycm;
   uint64_t Sy = 0, Syw = 0;
   bool ylists = false;
+  // exclusion lists: row v's sorted entries without its strongest parent
+  // (candidate bit xbit[v]); walked instead of the row when that parent is
+  // not a predecessor [n][Sxw]
+  DevBuf<double> xeff;
+  DevBuf<uint64_t> xcm;
+  DevBuf<uint64_t> xbit;
+  uint64_t Sx = 0, Sxw = 0;
+  bool xlists = false;
   int ylist_mode = -1;  // -1 auto (when they fit), 0 off, 1 on
   bool sorted_valid = false;
   float sort_ms = 0.f;
@@ -459,19 +467,23 @@ TieCtx tie_ctx(const bnmc_table* t) {
 // that contain q, in sorted order (ordered stream compaction, one CTA per
 // (q, v)), padded with never-admissible entries. Each list holds S(n-2, s-1)
 // entries; *err is set on a count mismatch.
+// Exclusion lists (xbit != null): one CTA per row v keeps the sorted entries
+// WITHOUT candidate bit xbit[v] (S(n-2, s) of them) into list v.
 constexpr int kYThreads = 256, kYItems = 4;
 __global__ void __launch_bounds__(kYThreads) ylist_build_kernel(
     const double* __restrict__ seff, const uint64_t* __restrict__ scm, uint64_t S, uint64_t Sw,
-    int n, double* yeff, uint64_t* ycm, uint64_t Sy, uint64_t Syw, int* err) {
+    int n, double* yeff, uint64_t* ycm, uint64_t Sy, uint64_t Syw, int* err,
+    const uint64_t* __restrict__ xbit = nullptr) {
   const int q = blockIdx.x, v = blockIdx.y;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   __shared__ uint32_t s_warp[kYThreads / 32 + 1];
   const double* re = seff + (uint64_t)v * Sw;
   const uint64_t* rc = scm + (uint64_t)v * Sw;
-  const uint64_t lo = ((uint64_t)v * (n - 1) + q) * Syw;
+  const uint64_t lo = xbit ? (uint64_t)v * Syw : ((uint64_t)v * (n - 1) + q) * Syw;
   double* oe = yeff + lo;
   uint64_t* oc = ycm + lo;
-  const uint64_t bit = 1ull << q;
+  const uint64_t bit = xbit ? xbit[v] : 1ull << q;
+  const uint64_t want = xbit ? 0ull : bit;  // keep entries whose (m & bit) == want
   uint64_t out = 0;
   for (uint64_t c0 = 0; c0 < S; c0 += (uint64_t)kYThreads * kYItems) {
     double e[kYItems];
@@ -482,7 +494,7 @@ __global__ void __launch_bounds__(kYThreads) ylist_build_kernel(
       const uint64_t i = c0 + (uint64_t)tid * kYItems + k;
       m[k] = i < S ? rc[i] : 0;
       e[k] = i < S ? re[i] : 0.0;
-      cnt += (m[k] & bit) ? 1u : 0u;
+      cnt += i < S && (m[k] & bit) == want ? 1u : 0u;
     }
     // exclusive prefix of the per-thread counts over the CTA (warp scan + warp sums)
     uint32_t incl = cnt;
@@ -505,7 +517,7 @@ __global__ void __launch_bounds__(kYThreads) ylist_build_kernel(
     uint64_t pos = out + s_warp[warp] + incl - cnt;
 #pragma unroll
     for (int k = 0; k < kYItems; ++k)
-      if (m[k] & bit) {
+      if (c0 + (uint64_t)tid * kYItems + k < S && (m[k] & bit) == want) {
         if (pos < Sy) {
           oe[pos] = e[k];
           oc[pos] = m[k];
@@ -660,6 +672,45 @@ void ensure_sorted(bnmc_table* t) {
     t->yeff.release();
     t->ycm.release();
   }
+  // exclusion lists: strongest parent of row v = the candidate most frequent
+  // among the row's top 256 sorted entries (a heuristic: results are exact
+  // for any choice, only walk lengths change)
+  t->Sx = t->n >= 2 ? bounded_count(t->n - 2, t->s) : 0;
+  t->Sxw = (t->Sx + 32 * kWalkPadRound + 31) / 32 * 32;
+  const uint64_t xbytes = static_cast<uint64_t>(t->n) * t->Sxw * 16;
+  CK(cudaMemGetInfo(&free_b, &total_b));
+  const char* xdis = std::getenv("BNMC_NO_XLISTS");
+  t->xlists = t->Sx > 0 && t->s >= 1 && !(xdis && xdis[0] == '1') && xbytes < free_b / 3;
+  if (t->xlists) {
+    const int top = static_cast<int>(std::min<uint64_t>(256, t->S));
+    std::vector<uint64_t> tops(static_cast<size_t>(t->n) * top), bits(t->n);
+    CK(cudaMemcpy2DAsync(tops.data(), top * 8, t->scm.p, t->Sw * 8, top * 8, t->n,
+                         cudaMemcpyDeviceToHost, t->stream));
+    CK(cudaStreamSynchronize(t->stream));
+    for (int v = 0; v < t->n; ++v) {
+      int cnt[64] = {0};
+      for (int i = 0; i < top; ++i)
+        for (uint64_t m = tops[static_cast<size_t>(v) * top + i]; m; m &= m - 1)
+          ++cnt[__builtin_ctzll(m)];
+      int best = 0;
+      for (int q = 1; q < t->n - 1; ++q)
+        if (cnt[q] > cnt[best]) best = q;
+      bits[v] = 1ull << best;
+    }
+    t->xbit.alloc(t->n);
+    t->xeff.alloc(static_cast<size_t>(t->n) * t->Sxw);
+    t->xcm.alloc(static_cast<size_t>(t->n) * t->Sxw);
+    CK(cudaMemcpyAsync(t->xbit.p, bits.data(), 8ull * t->n, cudaMemcpyHostToDevice, t->stream));
+    ylist_build_kernel<<<dim3(1, t->n), kYThreads, 0, t->stream>>>(
+        t->seff.p, t->scm.p, t->S, t->Sw, t->n, t->xeff.p, t->xcm.p, t->Sx, t->Sxw,
+        t->rowcnt.p + 2 * t->n + 1, t->xbit.p);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(t->stream));  // `bits` dies here
+  } else {
+    t->xeff.release();
+    t->xcm.release();
+    t->xbit.release();
+  }
   CK(cudaEventRecord(e1, t->stream));
   CK(cudaEventSynchronize(e1));
   CK(cudaEventElapsedTime(&t->sort_ms, e0, e1));
@@ -744,6 +795,11 @@ WalkArgs walk_args(bnmc_table* t) {
   A.ycm = t->ylists ? t->ycm.p : nullptr;
   A.Sy = t->Sy;
   A.Syw = t->Syw;
+  A.xeff = t->xlists ? t->xeff.p : nullptr;
+  A.xcm = t->xlists ? t->xcm.p : nullptr;
+  A.xbit = t->xlists ? t->xbit.p : nullptr;
+  A.Sx32 = static_cast<uint32_t>(t->Sx);
+  A.Sxw32 = static_cast<uint32_t>(t->Sxw);
   A.ls = t->ls.p;
   A.w = t->w.p;
   A.pst = t->pst.p;
@@ -754,7 +810,7 @@ WalkArgs walk_args(bnmc_table* t) {
   A.pc = t->pc;
   A.wbud = t->walk_budget;
   A.S = t->S;
-  if (t->Sw > 0xFFFFFFFFull || t->Syw > 0xFFFFFFFFull)  // unreachable within device memory
+  if (t->Sw > 0xFFFFFFFFull || t->Syw > 0xFFFFFFFFull || t->Sxw > 0xFFFFFFFFull)
     raise(BNMC_CAPACITY, "sorted rows longer than 2^32 entries");
   A.S32 = static_cast<uint32_t>(t->S);
   A.Sw32 = static_cast<uint32_t>(t->Sw);

@@ -87,6 +87,10 @@ struct WalkArgs {
   const double* __restrict__ yeff;    // [n][n-1][Syw] sorted entries of row v containing
   const uint64_t* __restrict__ ycm;   //   candidate q (delta walks), or null
   uint64_t Sy, Syw;                   // entries per list, padded stride
+  const double* __restrict__ xeff;    // [n][Sxw] row v without its strongest parent
+  const uint64_t* __restrict__ xcm;   //   (candidate bit xbit[v]), sorted, or null
+  const uint64_t* __restrict__ xbit;  // [n]
+  uint32_t Sx32, Sxw32;               // S(n-2, s), padded stride
   const double* __restrict__ ls;      // [n][S] local scores, BNSC order
   const double* __restrict__ w;       // [n][n] PPF weights
   const uint64_t* __restrict__ pst;   // position masks of PST(p) for p <= pc, concatenated
@@ -412,11 +416,14 @@ __device__ PairOut pair_argmax(const WalkArgs& A, int v, int p, uint64_t cpred, 
       return r;
     }
     // ---- walk of the sorted row; rows with a PST(p) stop after the budget
-    // and enumerate instead
-    const uint64_t ro = (uint64_t)(uint32_t)v * A.Sw32;
-    const double* re = A.seff + ro;
-    const uint64_t* rc = A.scm + ro;
-    const uint32_t S = A.S32;
+    // and enumerate instead. When the row's strongest parent is not a
+    // predecessor, no admissible set contains it: walk the row's exclusion
+    // list (same admissible entries in the same order, the others skipped).
+    const bool ex = A.xeff && (ncp & __ldg(A.xbit + v));
+    const uint64_t ro = (uint64_t)(uint32_t)v * (ex ? A.Sxw32 : A.Sw32);
+    const double* re = (ex ? A.xeff : A.seff) + ro;
+    const uint64_t* rc = (ex ? A.xcm : A.scm) + ro;
+    const uint32_t S = ex ? A.Sx32 : A.S32;
     const uint32_t lim =
         p <= A.pc ? (uint32_t)min((uint64_t)S, (uint64_t)A.wbud * (A.pst_off[p + 1] - A.pst_off[p])) : S;
     WalkHit h;
