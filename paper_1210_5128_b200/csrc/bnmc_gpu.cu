@@ -189,11 +189,12 @@ struct bnmc_table {
   // exclusion lists: row v's sorted entries without its strongest parent
   // (candidate bit xbit[v]); walked instead of the row when that parent is
   // not a predecessor [n][Sxw]
+  // level j = 1..xlev excludes the row's j strongest parents (nested)
   DevBuf<double> xeff;
   DevBuf<uint64_t> xcm;
-  DevBuf<uint64_t> xbit;
-  uint64_t Sx = 0, Sxw = 0;
-  bool xlists = false;
+  DevBuf<uint64_t> xbit;  // [n][kXLevels] candidate bits of the strongest parents
+  uint64_t Sx[kXLevels + 1] = {}, Sxw[kXLevels + 1] = {}, xoff[kXLevels + 1] = {};
+  int xlev = 0;
   int ylist_mode = -1;  // -1 auto (when they fit), 0 off, 1 on
   bool sorted_valid = false;
   float sort_ms = 0.f;
@@ -672,18 +673,31 @@ void ensure_sorted(bnmc_table* t) {
     t->yeff.release();
     t->ycm.release();
   }
-  // exclusion lists: strongest parent of row v = the candidate most frequent
-  // among the row's top 256 sorted entries (a heuristic: results are exact
-  // for any choice, only walk lengths change)
-  t->Sx = t->n >= 2 ? bounded_count(t->n - 2, t->s) : 0;
-  t->Sxw = (t->Sx + 32 * kWalkPadRound + 31) / 32 * 32;
-  const uint64_t xbytes = static_cast<uint64_t>(t->n) * t->Sxw * 16;
+  // exclusion lists: the row's strongest parents = the candidates most
+  // frequent among its top 256 sorted entries (a heuristic: results are exact
+  // for any choice, only walk lengths change); level j keeps the entries
+  // without any of the j strongest, S(n-1-j, s) of them
+  t->xlev = 0;
+  const char* xdis = std::getenv("BNMC_XLISTS");  // levels (default kXLevels), 0 = off
+  const int want_lev = std::min(kXLevels, xdis ? std::atoi(xdis) : kXLevels);
+  uint64_t xtotal = 0;
   CK(cudaMemGetInfo(&free_b, &total_b));
-  const char* xdis = std::getenv("BNMC_NO_XLISTS");
-  t->xlists = t->Sx > 0 && t->s >= 1 && !(xdis && xdis[0] == '1') && xbytes < free_b / 3;
-  if (t->xlists) {
+  for (int j = 1; j <= want_lev && t->s >= 1 && t->n - 1 - j >= 0; ++j) {
+    const uint64_t Sx = bounded_count(t->n - 1 - j, t->s);
+    const uint64_t Sxw = (Sx + 32 * kWalkPadRound + 31) / 32 * 32;
+    const uint64_t add = static_cast<uint64_t>(t->n) * Sxw;
+    if ((xtotal + add) * 16 >= free_b / 3) break;
+    t->Sx[j] = Sx;
+    t->Sxw[j] = Sxw;
+    t->xoff[j] = xtotal;
+    xtotal += add;
+    t->xlev = j;
+  }
+  if (t->xlev > 0) {
     const int top = static_cast<int>(std::min<uint64_t>(256, t->S));
-    std::vector<uint64_t> tops(static_cast<size_t>(t->n) * top), bits(t->n);
+    std::vector<uint64_t> tops(static_cast<size_t>(t->n) * top);
+    std::vector<uint64_t> bits(static_cast<size_t>(t->n) * kXLevels, 0);
+    std::vector<uint64_t> masks(static_cast<size_t>(t->n) * t->xlev);
     CK(cudaMemcpy2DAsync(tops.data(), top * 8, t->scm.p, t->Sw * 8, top * 8, t->n,
                          cudaMemcpyDeviceToHost, t->stream));
     CK(cudaStreamSynchronize(t->stream));
@@ -692,20 +706,31 @@ void ensure_sorted(bnmc_table* t) {
       for (int i = 0; i < top; ++i)
         for (uint64_t m = tops[static_cast<size_t>(v) * top + i]; m; m &= m - 1)
           ++cnt[__builtin_ctzll(m)];
-      int best = 0;
-      for (int q = 1; q < t->n - 1; ++q)
-        if (cnt[q] > cnt[best]) best = q;
-      bits[v] = 1ull << best;
+      uint64_t acc = 0;
+      for (int j = 0; j < t->xlev; ++j) {
+        int best = -1;  // most frequent candidate not taken yet (ties: lowest)
+        for (int q = 0; q < t->n - 1; ++q)
+          if (!((acc >> q) & 1) && (best < 0 || cnt[q] > cnt[best])) best = q;
+        bits[static_cast<size_t>(v) * kXLevels + j] = 1ull << best;
+        acc |= 1ull << best;
+        masks[static_cast<size_t>(j) * t->n + v] = acc;
+      }
     }
-    t->xbit.alloc(t->n);
-    t->xeff.alloc(static_cast<size_t>(t->n) * t->Sxw);
-    t->xcm.alloc(static_cast<size_t>(t->n) * t->Sxw);
-    CK(cudaMemcpyAsync(t->xbit.p, bits.data(), 8ull * t->n, cudaMemcpyHostToDevice, t->stream));
-    ylist_build_kernel<<<dim3(1, t->n), kYThreads, 0, t->stream>>>(
-        t->seff.p, t->scm.p, t->S, t->Sw, t->n, t->xeff.p, t->xcm.p, t->Sx, t->Sxw,
-        t->rowcnt.p + 2 * t->n + 1, t->xbit.p);
-    CK(cudaGetLastError());
-    CK(cudaStreamSynchronize(t->stream));  // `bits` dies here
+    t->xbit.alloc(bits.size());
+    t->xeff.alloc(xtotal);
+    t->xcm.alloc(xtotal);
+    DevBuf<uint64_t> d_masks;
+    d_masks.alloc(masks.size());
+    CK(cudaMemcpyAsync(t->xbit.p, bits.data(), 8 * bits.size(), cudaMemcpyHostToDevice, t->stream));
+    CK(cudaMemcpyAsync(d_masks.p, masks.data(), 8 * masks.size(), cudaMemcpyHostToDevice,
+                       t->stream));
+    for (int j = 1; j <= t->xlev; ++j) {
+      ylist_build_kernel<<<dim3(1, t->n), kYThreads, 0, t->stream>>>(
+          t->seff.p, t->scm.p, t->S, t->Sw, t->n, t->xeff.p + t->xoff[j], t->xcm.p + t->xoff[j],
+          t->Sx[j], t->Sxw[j], t->rowcnt.p + 2 * t->n + 1, d_masks.p + (j - 1) * t->n);
+      CK(cudaGetLastError());
+    }
+    CK(cudaStreamSynchronize(t->stream));  // host vectors and d_masks die here
   } else {
     t->xeff.release();
     t->xcm.release();
@@ -795,11 +820,15 @@ WalkArgs walk_args(bnmc_table* t) {
   A.ycm = t->ylists ? t->ycm.p : nullptr;
   A.Sy = t->Sy;
   A.Syw = t->Syw;
-  A.xeff = t->xlists ? t->xeff.p : nullptr;
-  A.xcm = t->xlists ? t->xcm.p : nullptr;
-  A.xbit = t->xlists ? t->xbit.p : nullptr;
-  A.Sx32 = static_cast<uint32_t>(t->Sx);
-  A.Sxw32 = static_cast<uint32_t>(t->Sxw);
+  A.xeff = t->xlev ? t->xeff.p : nullptr;
+  A.xcm = t->xlev ? t->xcm.p : nullptr;
+  A.xbit = t->xlev ? t->xbit.p : nullptr;
+  A.xlev = t->xlev;
+  for (int j = 0; j <= kXLevels; ++j) {
+    A.xoff[j] = t->xoff[j];
+    A.Sx32[j] = static_cast<uint32_t>(t->Sx[j]);
+    A.Sxw32[j] = static_cast<uint32_t>(t->Sxw[j]);
+  }
   A.ls = t->ls.p;
   A.w = t->w.p;
   A.pst = t->pst.p;
@@ -810,7 +839,7 @@ WalkArgs walk_args(bnmc_table* t) {
   A.pc = t->pc;
   A.wbud = t->walk_budget;
   A.S = t->S;
-  if (t->Sw > 0xFFFFFFFFull || t->Syw > 0xFFFFFFFFull || t->Sxw > 0xFFFFFFFFull)
+  if (t->Sw > 0xFFFFFFFFull || t->Syw > 0xFFFFFFFFull)
     raise(BNMC_CAPACITY, "sorted rows longer than 2^32 entries");
   A.S32 = static_cast<uint32_t>(t->S);
   A.Sw32 = static_cast<uint32_t>(t->Sw);

@@ -70,6 +70,7 @@ constexpr uint64_t kWalkCapDiv = 512;
 // 13.4M vs 9.0M it/s), shorter rows 4 (cfg4: 100M vs 91M it/s).
 constexpr uint64_t kDeepRowEntries = 1ull << 21;
 constexpr uint64_t kWalkBudget = BNMC_WALK_BUDGET_DEFAULT;
+constexpr int kXLevels = 3;  // nested exclusion lists per row (strongest parents)
 constexpr int kErrDrift = 7;  // error flag: debug_recheck found a drifted chain total
 constexpr uint64_t kRecheckEvery = 100;  // sampler.cpp:105
 
@@ -87,10 +88,12 @@ struct WalkArgs {
   const double* __restrict__ yeff;    // [n][n-1][Syw] sorted entries of row v containing
   const uint64_t* __restrict__ ycm;   //   candidate q (delta walks), or null
   uint64_t Sy, Syw;                   // entries per list, padded stride
-  const double* __restrict__ xeff;    // [n][Sxw] row v without its strongest parent
-  const uint64_t* __restrict__ xcm;   //   (candidate bit xbit[v]), sorted, or null
-  const uint64_t* __restrict__ xbit;  // [n]
-  uint32_t Sx32, Sxw32;               // S(n-2, s), padded stride
+  const double* __restrict__ xeff;    // exclusion lists, level j at xoff[j]: [n][Sxw[j]]
+  const uint64_t* __restrict__ xcm;   //   row v without its j strongest parents, or null
+  const uint64_t* __restrict__ xbit;  // [n][kXLevels] candidate bits of those parents
+  int xlev;                           // levels built (0..kXLevels)
+  uint64_t xoff[kXLevels + 1];
+  uint32_t Sx32[kXLevels + 1], Sxw32[kXLevels + 1];  // S(n-1-j, s), padded stride
   const double* __restrict__ ls;      // [n][S] local scores, BNSC order
   const double* __restrict__ w;       // [n][n] PPF weights
   const uint64_t* __restrict__ pst;   // position masks of PST(p) for p <= pc, concatenated
@@ -419,11 +422,23 @@ __device__ PairOut pair_argmax(const WalkArgs& A, int v, int p, uint64_t cpred, 
     // and enumerate instead. When the row's strongest parent is not a
     // predecessor, no admissible set contains it: walk the row's exclusion
     // list (same admissible entries in the same order, the others skipped).
-    const bool ex = A.xeff && (ncp & __ldg(A.xbit + v));
-    const uint64_t ro = (uint64_t)(uint32_t)v * (ex ? A.Sxw32 : A.Sw32);
-    const double* re = (ex ? A.xeff : A.seff) + ro;
-    const uint64_t* rc = (ex ? A.xcm : A.scm) + ro;
-    const uint32_t S = ex ? A.Sx32 : A.S32;
+    int xj = 0;  // leading strongest parents missing from the predecessors
+    if (A.xeff)
+      while (xj < A.xlev && (ncp & __ldg(A.xbit + v * kXLevels + xj))) ++xj;
+    const double* re;
+    const uint64_t* rc;
+    uint32_t S;
+    if (xj) {
+      const uint64_t ro = A.xoff[xj] + (uint64_t)(uint32_t)v * A.Sxw32[xj];
+      re = A.xeff + ro;
+      rc = A.xcm + ro;
+      S = A.Sx32[xj];
+    } else {
+      const uint64_t ro = (uint64_t)(uint32_t)v * A.Sw32;
+      re = A.seff + ro;
+      rc = A.scm + ro;
+      S = A.S32;
+    }
     const uint32_t lim =
         p <= A.pc ? (uint32_t)min((uint64_t)S, (uint64_t)A.wbud * (A.pst_off[p + 1] - A.pst_off[p])) : S;
     WalkHit h;

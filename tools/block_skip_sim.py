@@ -144,3 +144,82 @@ print(f"exclusion of the top parent applies to {hit / newd.size:.3f} of rows; de
 pr2 = np.array([plain_rounds(x) for x in newd])
 print(f"plain walk on the chosen list: rounds/row {pr2[:, 0].mean():.2f} (was {pr[:, 0].mean():.2f}), "
       f"entries/row {pr2[:, 1].mean():.1f} (was {pr[:, 1].mean():.1f})")
+
+# Two levels: lists without t1, without t2 (second most frequent), without both.
+tops2 = []
+for v in range(n):
+    top = srt[v][:256]
+    freq = np.array([int(((top >> np.uint64(j)) & np.uint64(1)).sum()) for j in range(c)])
+    o = np.argsort(-freq, kind="stable")
+    tops2.append((int(o[0]), int(o[1])))
+rng = np.random.default_rng(0)
+d1, d2 = [], []
+for perm in b.final_order:
+    for _ in range(props):
+        a_, b_ = sorted(rng.choice(n, 2, replace=False))
+        pp = np.array(perm).copy()
+        pp[a_], pp[b_] = pp[b_], pp[a_]
+        for p in range(a_, b_ + 1):
+            v = int(pp[p])
+            cp = 0
+            for u in pp[:p]:
+                u = int(u)
+                cp |= 1 << (u if u < v else u - 1)
+            adm = (srt[v] & ~np.uint64(cp)) == 0
+            dep = int(np.argmax(adm))
+            t1, t2 = tops2[v]
+            m1, m2 = not (cp >> t1) & 1, not (cp >> t2) & 1
+            has1 = ((srt[v][:dep + 1] >> np.uint64(t1)) & np.uint64(1)).astype(bool)
+            has2 = ((srt[v][:dep + 1] >> np.uint64(t2)) & np.uint64(1)).astype(bool)
+            # single level with two lists (t1 preferred)
+            if m1:
+                a = int((~has1).sum())
+            elif m2:
+                a = int((~has2).sum())
+            else:
+                a = dep + 1
+            # plus the double list
+            if m1 and m2:
+                bb = int((~(has1 | has2)).sum())
+            else:
+                bb = a
+            d1.append(a)
+            d2.append(bb)
+d1, d2 = np.array(d1), np.array(d2)
+for name, dd in (("t1 | t2 lists", d1), ("+ t1&t2 list", d2)):
+    pr3 = np.array([plain_rounds(x) for x in dd])
+    print(f"{name}: depth mean {dd.mean():.1f}, rounds/row {pr3[:, 0].mean():.2f}, "
+          f"entries/row {pr3[:, 1].mean():.1f}")
+
+# Nested exclusion lists: without {t1..tj}, j = 1..J; the walk takes the largest
+# j whose parents t1..tj are all missing from the predecessors.
+topsk = []
+for v in range(n):
+    top = srt[v][:256]
+    freq = np.array([int(((top >> np.uint64(j)) & np.uint64(1)).sum()) for j in range(c)])
+    topsk.append([int(x) for x in np.argsort(-freq, kind="stable")[:4]])
+for J in (1, 2, 3, 4):
+    rng = np.random.default_rng(0)
+    dd = []
+    for perm in b.final_order:
+        for _ in range(props):
+            a_, b_ = sorted(rng.choice(n, 2, replace=False))
+            pp = np.array(perm).copy()
+            pp[a_], pp[b_] = pp[b_], pp[a_]
+            for p in range(a_, b_ + 1):
+                v = int(pp[p])
+                cp = 0
+                for u in pp[:p]:
+                    u = int(u)
+                    cp |= 1 << (u if u < v else u - 1)
+                adm = (srt[v] & ~np.uint64(cp)) == 0
+                dep = int(np.argmax(adm))
+                j = 0
+                while j < J and not (cp >> topsk[v][j]) & 1:
+                    j += 1
+                ex = np.uint64(sum(1 << t for t in topsk[v][:j]))
+                dd.append(int(((srt[v][:dep + 1] & ex) == 0).sum()))
+    dd = np.array(dd)
+    pr3 = np.array([plain_rounds(x) for x in dd])
+    print(f"nested J={J}: depth mean {dd.mean():.1f}, rounds/row {pr3[:, 0].mean():.2f}, "
+          f"entries/row {pr3[:, 1].mean():.1f}")
