@@ -16,7 +16,8 @@ raw = list(csv.reader(io.StringIO(subprocess.run(["ncu", "-i", rep, "--page", "r
                                                  capture_output=True, text=True).stdout)))
 h, u, v = raw[0], raw[1], raw[2]
 scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "inst": 1, "%": 1,
-         "msecond": 1e-3, "usecond": 1e-6, "nsecond": 1e-9, "second": 1}
+         "msecond": 1e-3, "usecond": 1e-6, "nsecond": 1e-9, "second": 1,
+         "ms": 1e-3, "us": 1e-6, "ns": 1e-9, "s": 1}
 
 
 def get(k):
