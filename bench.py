@@ -308,8 +308,23 @@ def full_scan_probe(P, _lib, cache, pri, cfg, chains=64, iters=100):
     bpl = s_.value * 16.0 / launches  # 16-byte key slots streamed by K2
     avg = t.value / 1e3
     peak, src = load_peaks()
+    # OrderScorer::score of single orders (all n rows, one pair each) through K2
+    # alone, cold L2 before every launch: the north-star "order-score scan" bar
+    rng = np.random.default_rng(0)
+    one = {}
+    for cnt in (1, 8):
+        perms = np.stack([rng.permutation(cache.n()) for _ in range(cnt)]).astype(np.int32)
+        ms, kb = C.c_float(), C.c_uint64()
+        _lib.check(_lib.lib().bnmc_gpu_bench_scan(cache.handle, perms.ravel(), cnt, 0,
+                                                  cache.n() - 1, 20, 1, C.byref(ms), C.byref(kb)))
+        one[f"orders_{cnt}"] = {"avg_launch_us": ms.value * 1e3, "key_bytes": kb.value,
+                                "achieved_GBps": kb.value / (ms.value / 1e3) / 1e9,
+                                "frac": kb.value / (ms.value / 1e3) / 1e9 / peak}
     return {"it_s": chains * iters / (b.device_ms / 1e3), "chains": chains, "iterations": iters,
-            "kernel": "scan2_kernel (K2, full-row fp32-key scan)",
+            "kernel": "scan3_kernel (K2, streaming full-row fp32-key scan)",
+            "order_scan_cold": dict(one, note="full-order scans (every row rescanned) timed alone with "
+                                    "CUDA events after a 256 MiB L2 flush; key_bytes = 16-byte key "
+                                    "slots actually loaded (sector skipping) per launch"),
             "roofline": {"bound": "hbm", "achieved": bpl / avg / 1e9, "peak": peak, "unit": "GB/s",
                          "frac": bpl / avg / 1e9 / peak, "bytes_per_launch": bpl,
                          "avg_launch_us": avg * 1e6, "peak_source": src,

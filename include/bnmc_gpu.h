@@ -298,10 +298,13 @@ int bnmc_gpu_last_walk_variant(const bnmc_table* t, int* team_warps, int* entrie
  * glibc acceptance thresholds (an mh_accept decision fell inside the bound). */
 int bnmc_gpu_last_replayed(const bnmc_table* t, uint64_t* chains);
 
-/* Diagnostics: time the order-scan kernel alone on the rows at positions
- * lo..hi of `count` (<= 64) orders, averaged over `reps` launches (ms). */
+/* Diagnostics: time the order-scan kernel (K2) alone on the rows at positions
+ * lo..hi of `count` (<= 64) orders: `reps` launches, each timed with CUDA
+ * events and, when flush_l2 != 0, preceded by a 256 MiB write (cold L2).
+ * Outputs the mean launch time (ms) and the key bytes streamed per launch
+ * (16-byte slots actually loaded x 16; may be NULL). */
 int bnmc_gpu_bench_scan(bnmc_table* t, const int* perms, int count, int lo, int hi, int reps,
-                        float* ms_per_launch);
+                        int flush_l2, float* ms_per_launch, uint64_t* key_bytes_per_launch);
 
 #ifdef __cplusplus
 }

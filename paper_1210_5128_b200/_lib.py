@@ -79,8 +79,8 @@ SIGNATURES = {
     "bnmc_gpu_last_replayed": (C.c_int, [_vp, C.POINTER(C.c_uint64)]),
     "bnmc_gpu_last_walk_variant": (C.c_int, [_vp, C.POINTER(C.c_int), C.POINTER(C.c_int),
                                              C.POINTER(C.c_int)]),
-    "bnmc_gpu_bench_scan": (C.c_int, [_vp, _i32p, C.c_int, C.c_int, C.c_int, C.c_int,
-                                      C.POINTER(C.c_float)]),
+    "bnmc_gpu_bench_scan": (C.c_int, [_vp, _i32p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                      C.POINTER(C.c_float), C.POINTER(C.c_uint64)]),
     "bnmc_gpu_k1_partition": (C.c_int, [_i32p, C.c_uint64, C.c_int, C.c_int, C.c_int, _u64p]),
     "bnmc_gpu_table_build_part": (C.c_int, [_u8p, _i32p, C.c_uint64, C.c_int,
                                             C.POINTER(ScoreParams), _vp, C.c_int, C.c_int,
@@ -206,6 +206,14 @@ def pinned_empty(shape, dtype) -> np.ndarray:
         out = _vp()
         check(lib().bnmc_gpu_host_alloc(nbytes, C.byref(out)))
         ptr = out.value
+        # a caller looping `r = run_chains(...)` holds the previous result while
+        # the next call fills new buffers: keep a second block of this size
+        # pooled so the steady state never allocates page-locked memory
+        if _POOL_BYTES[0] + nbytes <= _POOL_CAP:
+            spare = _vp()
+            check(lib().bnmc_gpu_host_alloc(nbytes, C.byref(spare)))
+            _POOL.setdefault(nbytes, []).append(spare.value)
+            _POOL_BYTES[0] += nbytes
     buf = (C.c_char * nbytes).from_address(ptr)
     weakref.finalize(buf, _release, ptr, nbytes)
     return np.frombuffer(buf, dtype=dtype, count=count).reshape(shape)

@@ -589,11 +589,22 @@ class ChainBatch:
     def allocate(cls, chains: int, iterations: int, n: int, track_top: int, pinned: bool = True):
         """Result buffers for `chains` chains; page-locked (bnmc_gpu_host_alloc,
         pooled) unless pinned=False."""
-        E = _lib.pinned_empty if pinned else (lambda shape, dt: np.empty(shape, dt))
         c, i, K = chains, iterations, track_top
-        return cls(E((c, i), np.float64), E((c, i), np.uint8), E((c, i), np.float64),
-                   E((c, n), np.int32), E((c,), np.float64), E((c,), np.uint64),
-                   E((c,), np.int32), E((c, K, n), np.uint64), E((c, K), np.float64), 0.0, 0.0)
+        shapes = [((c, i), np.float64), ((c, i), np.uint8), ((c, i), np.float64),
+                  ((c, n), np.int32), ((c,), np.float64), ((c,), np.uint64),
+                  ((c,), np.int32), ((c, K, n), np.uint64), ((c, K), np.float64)]
+        if not pinned:
+            return cls(*[np.empty(sh, dt) for sh, dt in shapes], 0.0, 0.0)
+        # one page-locked block per batch (64-byte aligned views): one pool entry,
+        # so a reused batch size never allocates page-locked memory again
+        offs, total = [], 0
+        for sh, dt in shapes:
+            offs.append(total)
+            total += (int(np.prod(sh)) * np.dtype(dt).itemsize + 63) // 64 * 64
+        block = _lib.pinned_empty((total,), np.uint8)
+        views = [block[o:o + int(np.prod(sh)) * np.dtype(dt).itemsize].view(dt).reshape(sh)
+                 for o, (sh, dt) in zip(offs, shapes)]
+        return cls(*views, 0.0, 0.0)
 
     def result(self, c: int, seed: int = 0) -> McmcResult:
         """McmcResult of chain c as views into the batch buffers (no copies)."""

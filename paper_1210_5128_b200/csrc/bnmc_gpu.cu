@@ -261,34 +261,76 @@ constexpr int kMaxChainsPerLaunch = 64;
 
 struct ScanGeom {
   int G, sectors;
+  int kernel;  // 2: scan2 (row groups), 3: scan3 (streaming, default)
+  int E, D, T;  // scan3: entries per thread, rows in flight per thread, CTA threads
 };
 
-// CTA b owns Ls <= 512 consecutive sectors of every row (one CTA per SM when
-// the row fits), RB rows per cp.async pipeline stage within the smem budget.
+// scan3: CTA b owns T*E consecutive global indices of every row.
+// BNMC_SCAN_KERNEL=2 selects the row-group kernel (A/B), BNMC_SCAN3="E,D,T" the
+// scan3 variant (see scan3_select).
 ScanGeom scan_geometry(const bnmc_table* t, int max_pairs) {
   ScanGeom g;
   (void)max_pairs;
   g.sectors = static_cast<int>(t->Sp / 8);
-  const uint64_t slots = (static_cast<uint64_t>(g.sectors) * 8 + kScan2Per - 1) / kScan2Per;
-  g.G = static_cast<int>((slots + kScan2Threads - 1) / kScan2Threads);
+  g.kernel = static_cast<int>(env_u64("BNMC_SCAN_KERNEL", 3));
+  g.E = 8;
+  g.D = 2;
+  g.T = 256;
+  if (const char* e = std::getenv("BNMC_SCAN3")) std::sscanf(e, "%d,%d,%d", &g.E, &g.D, &g.T);
+  if (g.kernel == 2) {
+    const uint64_t slots = (static_cast<uint64_t>(g.sectors) * 8 + kScan2Per - 1) / kScan2Per;
+    g.G = static_cast<int>((slots + kScan2Threads - 1) / kScan2Threads);
+  } else {
+    const uint64_t per_cta = static_cast<uint64_t>(g.T) * g.E;
+    g.G = static_cast<int>((t->Sp + per_cta - 1) / per_cta);
+  }
   return g;
 }
 
-// K2 (scan2_kernel): one thread per 32-byte key sector of every row.
+template <int E, int D, int T>
+void* scan3_fn() {
+  static bool init = false;
+  if (!init) {  // up to 64 chains x 64 rows x 24 B of pair state
+    CK(cudaFuncSetAttribute(scan3_kernel<E, D, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            24 * kMaxChains * kMaxNodes));
+    init = true;
+  }
+  return reinterpret_cast<void*>(scan3_kernel<E, D, T>);
+}
+
+void* scan3_select(int E, int D, int T) {
+  if (E == 8 && D == 2 && T == 256) return scan3_fn<8, 2, 256>();
+  if (E == 8 && D == 4 && T == 256) return scan3_fn<8, 4, 256>();
+  if (E == 8 && D == 2 && T == 128) return scan3_fn<8, 2, 128>();
+  if (E == 16 && D == 2 && T == 128) return scan3_fn<16, 2, 128>();
+  if (E == 16 && D == 2 && T == 256) return scan3_fn<16, 2, 256>();
+  if (E == 4 && D == 4 && T == 256) return scan3_fn<4, 4, 256>();
+  raise(BNMC_USAGE, "BNMC_SCAN3: unsupported (E,D,T)");
+  return nullptr;
+}
+
+// K2: scan2 (row groups) or scan3 (streaming) over the step's bucketed pairs.
 void launch_scan(const ScanGeom& g, ScanArgs a, int max_pairs, cudaStream_t s, bool pdl) {
   a.sectors = g.sectors;
-  (void)max_pairs;
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(g.G, kScan2RowGroups);
-  cfg.blockDim = dim3(kScan2Threads);
-  cfg.dynamicSmemBytes = 0;
-  cfg.stream = s;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  CK(cudaLaunchKernelEx(&cfg, scan2_kernel, a));
+  cfg.blockDim = dim3(g.kernel == 2 ? kScan2Threads : g.T);
+  cfg.stream = s;
+  if (g.kernel == 2) {
+    cfg.gridDim = dim3(g.G, kScan2RowGroups);
+    cfg.dynamicSmemBytes = 0;
+    CK(cudaLaunchKernelEx(&cfg, scan2_kernel, a));
+    return;
+  }
+  cfg.gridDim = dim3(g.G);
+  cfg.dynamicSmemBytes = 24ull * std::min(max_pairs, kMaxChains * kMaxNodes);
+  void* fn = scan3_select(g.E, g.D, g.T);
+  void* args[] = {&a};
+  CK(cudaLaunchKernelExC(&cfg, fn, args));
 }
 
 void launch_step(int C, const StepArgs& A, cudaStream_t s, bool pdl) {
@@ -1691,7 +1733,7 @@ int bnmc_gpu_score_orders(bnmc_table* t, const int* perms, int count, uint64_t* 
 }
 
 int bnmc_gpu_bench_scan(bnmc_table* t, const int* perms, int count, int lo, int hi, int reps,
-                        float* ms_per_launch) {
+                        int flush_l2, float* ms_per_launch, uint64_t* key_bytes_per_launch) {
   return guarded([&] {
     if (!t) raise(BNMC_USAGE, "null table");
     if (count < 1 || count > kMaxChainsPerLaunch) raise(BNMC_USAGE, "count must lie in [1,64]");
@@ -1708,16 +1750,29 @@ int bnmc_gpu_bench_scan(bnmc_table* t, const int* perms, int count, int lo, int 
     CK(cudaGetLastError());
     const ScanArgs sa = scan_args(t, g);
     launch_scan(g, sa, count * n, t->stream, false);  // warm-up
+    DevBuf<uint32_t> scratch;  // > L2 (126 MB): every timed launch starts cold
+    if (flush_l2) scratch.alloc(64ull << 20);
+    CK(cudaMemsetAsync(sa.sector_loads, 0, sizeof(unsigned long long), t->stream));
     cudaEvent_t e0, e1;
     CK(cudaEventCreate(&e0));
     CK(cudaEventCreate(&e1));
-    CK(cudaEventRecord(e0, t->stream));
-    for (int r = 0; r < reps; ++r) launch_scan(g, sa, count * n, t->stream, false);
-    CK(cudaEventRecord(e1, t->stream));
-    CK(cudaEventSynchronize(e1));
-    float ms = 0.f;
-    CK(cudaEventElapsedTime(&ms, e0, e1));
-    *ms_per_launch = ms / std::max(1, reps);
+    double total = 0.0;
+    for (int r = 0; r < std::max(1, reps); ++r) {
+      if (flush_l2) CK(cudaMemsetAsync(scratch.p, r & 0xff, 256ull << 20, t->stream));
+      CK(cudaEventRecord(e0, t->stream));
+      launch_scan(g, sa, count * n, t->stream, false);
+      CK(cudaEventRecord(e1, t->stream));
+      CK(cudaEventSynchronize(e1));
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, e0, e1));
+      total += ms;
+    }
+    *ms_per_launch = static_cast<float>(total / std::max(1, reps));
+    if (key_bytes_per_launch) {
+      unsigned long long slots = 0;
+      CK(cudaMemcpy(&slots, sa.sector_loads, sizeof(slots), cudaMemcpyDeviceToHost));
+      *key_bytes_per_launch = slots * 16ull / static_cast<uint64_t>(std::max(1, reps));
+    }
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
   });

@@ -49,6 +49,29 @@ __device__ __forceinline__ double ppf_sum(const double* __restrict__ w, int n, i
   return t;
 }
 
+// Exact x % d for a fixed divisor 2 <= d < 2^32 without a 64-bit division
+// (the generic one is ~100 instructions, issued every iteration by
+// propose_swap): m = floor((2^64 - 1) / d), q = umulhi(x, m) is floor(x / d)
+// minus at most 2, so at most two corrections. thr = (0 - d) % d is
+// next_below's rejection threshold (rng.hpp:31-38).
+struct FastDiv {
+  uint64_t d, m, thr;
+  __device__ __host__ static FastDiv make(uint64_t d) {
+    return FastDiv{d, ~0ull / d, (0 - d) % d};
+  }
+  __device__ __host__ uint64_t mod(uint64_t x) const {
+#ifdef __CUDA_ARCH__
+    const uint64_t q = __umul64hi(x, m);
+#else
+    const uint64_t q = (uint64_t)(((unsigned __int128)x * m) >> 64);
+#endif
+    uint64_t r = x - q * d;
+    if (r >= d) r -= d;
+    if (r >= d) r -= d;
+    return r;
+  }
+};
+
 // splitmix64 Rng (rng.hpp:14-45)
 struct Rng {
   uint64_t s;
@@ -71,6 +94,15 @@ struct Rng {
       x = next_u64();
     } while (x < threshold);
     return x % bound;
+  }
+  // next_below with a precomputed divisor (FastDiv): same draws, same results
+  template <class Div>
+  __device__ __host__ uint64_t next_below(const Div& d) {
+    uint64_t x;
+    do {
+      x = next_u64();
+    } while (x < d.thr);
+    return d.mod(x);
   }
   __device__ __host__ double next_unit_open() {
     return ((double)(next_u64() >> 11) + 0.5) * 0x1.0p-53;

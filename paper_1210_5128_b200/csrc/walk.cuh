@@ -666,10 +666,12 @@ __global__ void __launch_bounds__(walk_cta_threads<TW>(), TW == 1 ? kWalkMinBloc
   __shared__ uint64_t s_bt[65 * 9];
   __shared__ uint64_t s_boff[9];  // size-class offsets of global_index for c = n - 1
   __shared__ TeamState s_team[kTeams];
+  __shared__ FastDiv s_div[2];  // propose_swap's bounds n and n - 1
   const int tid = threadIdx.x, lane = tid & 31;
   const int team = (tid >> 5) / TW, twarp = (tid >> 5) % TW, ttid = tid - team * TW * 32;
   const int c = blockIdx.x * kTeams + team;
   const int n = A.n;
+  if (tid < 2) s_div[tid] = FastDiv::make((uint64_t)(n - tid));
   for (int i = tid; i < 65 * 9; i += kCta) s_bt[i] = binom(i / 9, i % 9);
   if (tid < 9) {
     uint64_t o = 0;
@@ -700,8 +702,8 @@ __global__ void __launch_bounds__(walk_cta_threads<TW>(), TW == 1 ? kWalkMinBloc
       int a = 0, b = n - 1;
       if (!BNMC_FRESH) {
         Rng pr{S.rng};
-        a = (int)pr.next_below((uint64_t)n);
-        b = (int)pr.next_below((uint64_t)(n - 1));
+        a = (int)pr.next_below(s_div[0]);
+        b = (int)pr.next_below(s_div[1]);
         if (b >= a) ++b;
         S.rng = pr.s;
         if (A.thr) {
@@ -958,6 +960,8 @@ __global__ void __launch_bounds__(1024, 1) walk_spec_kernel(WalkArgs A) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int c = blockIdx.x;
   const int n = A.n;
+  __shared__ FastDiv s_div[2];  // propose_swap's bounds n and n - 1
+  if (threadIdx.x < 2) s_div[threadIdx.x] = FastDiv::make((uint64_t)(n - threadIdx.x));
   for (int i = tid; i < 65 * 9; i += kThreads) s_bt[i] = binom(i / 9, i % 9);
   if (tid < 9) {
     uint64_t o = 0;
@@ -1004,8 +1008,8 @@ __global__ void __launch_bounds__(1024, 1) walk_spec_kernel(WalkArgs A) {
           S.b = n - 1;
           S.thr = 0.0;
         } else {
-          int a = (int)pr.next_below((uint64_t)n);  // propose_swap, sampler.cpp:43-52
-          int b = (int)pr.next_below((uint64_t)(n - 1));
+          int a = (int)pr.next_below(s_div[0]);  // propose_swap, sampler.cpp:43-52
+          int b = (int)pr.next_below(s_div[1]);
           if (b >= a) ++b;
           S.a = a;
           S.b = b;

@@ -9,7 +9,7 @@ for tool in memcheck racecheck synccheck; do
     extra=""
     [ $tool = memcheck ] && extra="--leak-check full"
     [ $tool = racecheck ] && extra="--racecheck-report all"
-    timeout 900 $CS --tool $tool $extra --print-limit 50 --error-exitcode 9 \
+    timeout 600 $CS --tool $tool $extra --print-limit 50 --error-exitcode 9 \
       python tools/sanitize_run.py $c > $D/${tool}_$c.log 2>&1
     echo "$tool $c rc=$?" | tee -a $D/summary.txt
   done
