@@ -321,11 +321,14 @@ def full_scan_probe(P, _lib, cache, pri, cfg, chains=64, iters=100):
                                 "achieved_GBps": kb.value / (ms.value / 1e3) / 1e9,
                                 "frac": kb.value / (ms.value / 1e3) / 1e9 / peak}
     return {"it_s": chains * iters / (b.device_ms / 1e3), "chains": chains, "iterations": iters,
-            "kernel": "scan3_kernel (K2, streaming full-row fp32-key scan)",
+            "kernel": "scan2_kernel (K2, full-row fp32-key scan)",
             "order_scan_cold": dict(one, note="full-order scans (every row rescanned) timed alone with "
                                     "CUDA events after a 256 MiB L2 flush; key_bytes = 16-byte key "
                                     "slots actually loaded (sector skipping) per launch"),
-            "roofline": {"bound": "hbm", "achieved": bpl / avg / 1e9, "peak": peak, "unit": "GB/s",
+            # measured bound: per-CTA latency chains (one order) and issue (many
+            # orders), not HBM (profiles/r02_ncu_scan2_c1.txt, K2)
+            "roofline": {"bound": "issue/latency", "achieved": bpl / avg / 1e9, "peak": peak,
+                         "unit": "GB/s",
                          "frac": bpl / avg / 1e9 / peak, "bytes_per_launch": bpl,
                          "avg_launch_us": avg * 1e6, "peak_source": src,
                          "row_equivalent_GBps": (a.value / launches) * cache.entries_per_node() * 4.0

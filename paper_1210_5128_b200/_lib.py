@@ -7,6 +7,7 @@ compute entry point is called, the call raises.
 """
 from __future__ import annotations
 
+import atexit
 import ctypes as C
 import os
 
@@ -179,11 +180,31 @@ def device_count() -> int:
 _POOL: dict = {}
 _POOL_BYTES = [0]
 _POOL_CAP = 8 << 30
+_EXITING = [False]
+
+
+def _drain_pool():
+    """At interpreter exit: return every pooled block to the driver (blocks
+    still referenced are freed by their finalizers, which see _EXITING)."""
+    _EXITING[0] = True
+    for ptrs in _POOL.values():
+        for p in ptrs:
+            try:
+                _lib.bnmc_gpu_host_free(p)
+            except Exception:
+                pass
+    _POOL.clear()
+    _POOL_BYTES[0] = 0
+
+
+atexit.register(_drain_pool)
 
 
 def _release(ptr: int, nbytes: int):
     try:
-        if _POOL_BYTES[0] + nbytes <= _POOL_CAP:
+        if _EXITING[0]:
+            _lib.bnmc_gpu_host_free(ptr)
+        elif _POOL_BYTES[0] + nbytes <= _POOL_CAP:
             _POOL.setdefault(nbytes, []).append(ptr)
             _POOL_BYTES[0] += nbytes
         elif _lib is not None:

@@ -261,76 +261,33 @@ constexpr int kMaxChainsPerLaunch = 64;
 
 struct ScanGeom {
   int G, sectors;
-  int kernel;  // 2: scan2 (row groups), 3: scan3 (streaming, default)
-  int E, D, T;  // scan3: entries per thread, rows in flight per thread, CTA threads
 };
 
-// scan3: CTA b owns T*E consecutive global indices of every row.
-// BNMC_SCAN_KERNEL=2 selects the row-group kernel (A/B), BNMC_SCAN3="E,D,T" the
-// scan3 variant (see scan3_select).
+// K2 (scan2_kernel): CTA (x, y) owns kScan2Threads x kScan2Per consecutive
+// global indices of the step's rows y, y + 8, ...
 ScanGeom scan_geometry(const bnmc_table* t, int max_pairs) {
   ScanGeom g;
   (void)max_pairs;
   g.sectors = static_cast<int>(t->Sp / 8);
-  g.kernel = static_cast<int>(env_u64("BNMC_SCAN_KERNEL", 3));
-  g.E = 8;
-  g.D = 2;
-  g.T = 256;
-  if (const char* e = std::getenv("BNMC_SCAN3")) std::sscanf(e, "%d,%d,%d", &g.E, &g.D, &g.T);
-  if (g.kernel == 2) {
-    const uint64_t slots = (static_cast<uint64_t>(g.sectors) * 8 + kScan2Per - 1) / kScan2Per;
-    g.G = static_cast<int>((slots + kScan2Threads - 1) / kScan2Threads);
-  } else {
-    const uint64_t per_cta = static_cast<uint64_t>(g.T) * g.E;
-    g.G = static_cast<int>((t->Sp + per_cta - 1) / per_cta);
-  }
+  const uint64_t slots = (static_cast<uint64_t>(g.sectors) * 8 + kScan2Per - 1) / kScan2Per;
+  g.G = static_cast<int>((slots + kScan2Threads - 1) / kScan2Threads);
   return g;
 }
 
-template <int E, int D, int T>
-void* scan3_fn() {
-  static bool init = false;
-  if (!init) {  // up to 64 chains x 64 rows x 24 B of pair state
-    CK(cudaFuncSetAttribute(scan3_kernel<E, D, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            24 * kMaxChains * kMaxNodes));
-    init = true;
-  }
-  return reinterpret_cast<void*>(scan3_kernel<E, D, T>);
-}
-
-void* scan3_select(int E, int D, int T) {
-  if (E == 8 && D == 2 && T == 256) return scan3_fn<8, 2, 256>();
-  if (E == 8 && D == 4 && T == 256) return scan3_fn<8, 4, 256>();
-  if (E == 8 && D == 2 && T == 128) return scan3_fn<8, 2, 128>();
-  if (E == 16 && D == 2 && T == 128) return scan3_fn<16, 2, 128>();
-  if (E == 16 && D == 2 && T == 256) return scan3_fn<16, 2, 256>();
-  if (E == 4 && D == 4 && T == 256) return scan3_fn<4, 4, 256>();
-  raise(BNMC_USAGE, "BNMC_SCAN3: unsupported (E,D,T)");
-  return nullptr;
-}
-
-// K2: scan2 (row groups) or scan3 (streaming) over the step's bucketed pairs.
 void launch_scan(const ScanGeom& g, ScanArgs a, int max_pairs, cudaStream_t s, bool pdl) {
   a.sectors = g.sectors;
+  (void)max_pairs;
   cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(g.G, kScan2RowGroups);
+  cfg.blockDim = dim3(kScan2Threads);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  cfg.blockDim = dim3(g.kernel == 2 ? kScan2Threads : g.T);
-  cfg.stream = s;
-  if (g.kernel == 2) {
-    cfg.gridDim = dim3(g.G, kScan2RowGroups);
-    cfg.dynamicSmemBytes = 0;
-    CK(cudaLaunchKernelEx(&cfg, scan2_kernel, a));
-    return;
-  }
-  cfg.gridDim = dim3(g.G);
-  cfg.dynamicSmemBytes = 24ull * std::min(max_pairs, kMaxChains * kMaxNodes);
-  void* fn = scan3_select(g.E, g.D, g.T);
-  void* args[] = {&a};
-  CK(cudaLaunchKernelExC(&cfg, fn, args));
+  CK(cudaLaunchKernelEx(&cfg, scan2_kernel, a));
 }
 
 void launch_step(int C, const StepArgs& A, cudaStream_t s, bool pdl) {

@@ -121,11 +121,6 @@ struct ScanArgs {
 // lane max over its 8 admissible keys, warp REDUX, shared 64-bit atomics per
 // CTA, one pair of global atomics per CTA and pair — the same (key, g) /
 // (key, ~g) cells and exact tie resolution in K3 as the v1 kernel.
-__device__ __forceinline__ void cell_flush(unsigned long long* cell, unsigned long long v) {
-  // most CTAs lose: a plain read filters the same-address atomic queue
-  if (v > *reinterpret_cast<volatile unsigned long long*>(cell)) atomicMax(cell, v);
-}
-
 constexpr int kScan2Threads = 256;
 #ifndef BNMC_SCAN2_PER
 #define BNMC_SCAN2_PER 8
@@ -215,44 +210,34 @@ __global__ void __launch_bounds__(kScan2Threads, kScan2Per > 8 ? 2 : 4) scan2_ke
     return true;
   };
   hn = fetch(0, kn);
-  uint64_t uni = 0;
-#pragma unroll
-  for (int e = 0; e < kScan2Per; ++e) uni |= m[e];
   for (int i = 0; i < myrows; ++i) {
     float k[kScan2Per];
 #pragma unroll
-    for (int e = 0; e < kScan2Per; ++e) k[e] = kn[e];
-    const bool hk = hn;
+    for (int e = 0; e < kScan2Per; ++e) k[e] = hn ? kn[e] : -INFINITY;  // unloaded: nothing admissible
     hn = fetch(i + 1, kn);
-    if (!__any_sync(0xffffffffu, hk)) continue;  // warp-uniform: no lane loaded this row
     const int v = s_rows[ry + i * RG];
     const int cnt = s_cnt[v];
     for (int q = 0; q < cnt; ++q) {
       const uint64_t ncp = ~a.buckets[(b * n + v) * kMaxChains + q].cpred;
       if ((winter & ncp) != 0) continue;  // warp-uniform: no entry of the warp admissible
-      // lane maximum: nothing when the sector was skipped or misses the set; no
-      // per-entry tests when every entry of the sector is admissible
-      float mx = -INFINITY;
-      if (hk && (inter & ncp) == 0) {
-        if ((uni & ncp) == 0) {
+      // branch-free lane max: inadmissible entries become -inf (keys are finite)
+      float kk[kScan2Per];
 #pragma unroll
-          for (int e = 0; e < kScan2Per; ++e) mx = fmaxf(mx, k[e]);
-        } else {
+      for (int e = 0; e < kScan2Per; ++e) kk[e] = (m[e] & ncp) == 0 ? k[e] : -INFINITY;
+      float mx = kk[0];
 #pragma unroll
-          for (int e = 0; e < kScan2Per; ++e) mx = fmaxf(mx, (m[e] & ncp) == 0 ? k[e] : -INFINITY);
-        }
-      }
+      for (int e = 1; e < kScan2Per; ++e) mx = fmaxf(mx, kk[e]);
       const uint32_t ko = mx != -INFINITY ? ordkey(mx) : 0u;
       const uint32_t mxw = __reduce_max_sync(0xffffffffu, ko);
-      // locate only when the warp can still raise or tie the CTA's cell
-      if (mxw != 0u && mxw >= (uint32_t)(*reinterpret_cast<volatile unsigned long long*>(&s_cell[i][q][0]) >> 32)) {
+      if (mxw != 0u) {
         // only the lanes holding the warp maximum locate it: first and last
         // entry with that key (they differ iff the lane itself holds a tie)
+        const bool win = ko == mxw;
         uint32_t glast = 0u, gfirst = 0xFFFFFFFFu;
-        if (ko == mxw) {
+        if (win) {
           uint32_t bits = 0;
 #pragma unroll
-          for (int e = 0; e < kScan2Per; ++e) bits |= ((m[e] & ncp) == 0 && k[e] == mx ? 1u : 0u) << e;
+          for (int e = 0; e < kScan2Per; ++e) bits |= (kk[e] == mx ? 1u : 0u) << e;
           gfirst = (uint32_t)g0 + (__ffs(bits) - 1);
           glast = (uint32_t)g0 + (31 - __clz(bits));
         }
@@ -275,188 +260,12 @@ __global__ void __launch_bounds__(kScan2Threads, kScan2Per > 8 ? 2 : 4) scan2_ke
       if (c0 != 0ull) {
         const PairRec pr = a.buckets[(b * n + v) * kMaxChains + q];
         unsigned long long* cell = a.cell + 2ull * (pr.chain * n + pr.slot);
-        cell_flush(cell, c0);
-        cell_flush(cell + 1, c1);
+        atomicMax(cell, c0);
+        atomicMax(cell + 1, c1);
       }
     }
   }
   if (a.sector_loads) {  // 16-byte key slots loaded
-    for (int off = 16; off > 0; off >>= 1) loads += __shfl_down_sync(0xffffffffu, loads, off);
-    if (lane == 0 && loads) atomicAdd(a.sector_loads, loads);
-  }
-}
-
-// ---------------------------------------------------------------------------
-// K2 v3 — streaming full-row scan. One CTA column owns 256·E consecutive
-// global indices of EVERY row of the step (no row groups): the candidate masks
-// are loaded once per launch (not once per row group), and each thread keeps
-// the keys of the next D rows in flight in a register ring while it reduces
-// the current row — 16·E·D bytes per thread outstanding with no barrier in
-// the row loop, which is what a single order (one pair per row, ~49 MB after
-// sector skipping) needs to run at HBM speed instead of at row-load latency.
-// Pairs' complemented predecessor sets and their (key, g) / (key, ~g) cells
-// live in dynamic shared memory indexed by the pair's rank in the step
-// (rows ascending, bucket order): 24 B per pair, sized by the host for the
-// launch's maximum (chains x n). Cells and tie semantics are scan2's, so the
-// step kernel is shared.
-
-
-template <int E, int D, int T>
-__global__ void __launch_bounds__(T) scan3_kernel(ScanArgs a) {
-  static_assert(E % 4 == 0 && E <= 16, "E: 4, 8 or 16 entries per thread");
-  extern __shared__ unsigned long long s_dyn[];
-  __shared__ int s_rows[kMaxNodes], s_cnt[kMaxNodes], s_off[kMaxNodes], s_nrows, s_q, s_sel;
-  __shared__ uint64_t s_union[kMaxNodes];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int n = a.n;
-  const uint64_t g0 = ((uint64_t)blockIdx.x * T + tid) * E;
-  const bool mine_ok = g0 < a.Sp;  // Sp is a multiple of 32: all E entries in range when E <= 32
-  uint64_t m[E];
-  uint64_t inter = ~0ull, uni = 0ull;
-  {
-    const ulonglong2* src = reinterpret_cast<const ulonglong2*>(a.tie.cmask + (mine_ok ? g0 : 0));
-#pragma unroll
-    for (int h = 0; h < E / 2; ++h) {
-      const ulonglong2 v2 = mine_ok ? __ldg(src + h) : make_ulonglong2(~0ull, ~0ull);
-      m[2 * h] = v2.x;
-      m[2 * h + 1] = v2.y;
-    }
-#pragma unroll
-    for (int e = 0; e < E; ++e) {
-      inter &= m[e];
-      uni |= m[e];
-    }
-  }
-  const uint64_t winter = ((uint64_t)__reduce_and_sync(0xffffffffu, (unsigned)(inter >> 32)) << 32) |
-                          __reduce_and_sync(0xffffffffu, (unsigned)inter);
-  cudaGridDependencySynchronize();
-  if (tid == 0) s_sel = *a.sel;
-  __syncthreads();
-  const int b = s_sel;
-  if (warp == 0) {  // compact rows with pairs, ascending; pair offsets by exclusive scan
-    int c[2];
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int v = 2 * lane + h;
-      c[h] = v < n ? a.rowcnt[b * n + v] : 0;
-    }
-    const unsigned b0 = __ballot_sync(0xffffffffu, c[0] > 0), b1 = __ballot_sync(0xffffffffu, c[1] > 0);
-    const unsigned below = (1u << lane) - 1u;
-    int pos = __popc(b0 & below) + __popc(b1 & below);
-    int incl = c[0] + c[1];
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += y;
-    }
-    int off = incl - c[0] - c[1];
-    if (c[0] > 0) { s_rows[pos] = 2 * lane; s_cnt[pos] = c[0]; s_off[pos] = off; ++pos; off += c[0]; }
-    if (c[1] > 0) { s_rows[pos] = 2 * lane + 1; s_cnt[pos] = c[1]; s_off[pos] = off; }
-    if (lane == 31) { s_nrows = __popc(b0) + __popc(b1); s_q = incl; }
-  }
-  __syncthreads();
-  const int nrows = s_nrows, Q = s_q;
-  uint64_t* s_ncp = reinterpret_cast<uint64_t*>(s_dyn);
-  unsigned long long* s_cell = s_dyn + Q;
-  for (int i = warp; i < nrows; i += T / 32) {  // pairs' sets + per-row union
-    const int v = s_rows[i], cnt = s_cnt[i], off = s_off[i];
-    uint64_t u = 0;
-    for (int j = lane; j < cnt; j += 32) {
-      const uint64_t p = a.buckets[(b * n + v) * kMaxChains + j].cpred;
-      s_ncp[off + j] = ~p;
-      u |= p;
-    }
-    for (int o = 16; o > 0; o >>= 1) u |= __shfl_xor_sync(0xffffffffu, u, o);
-    if (lane == 0) s_union[i] = u;
-  }
-  for (int i = tid; i < 2 * Q; i += T) s_cell[i] = 0ull;
-  __syncthreads();
-
-  unsigned long long loads = 0;
-  auto fetch = [&](int i, float* k) -> bool {
-    if (i >= nrows || !mine_ok) return false;
-    if ((inter & ~s_union[i]) != 0) return false;  // no entry admissible for any pair of the row
-    const float4* src = reinterpret_cast<const float4*>(a.keys + (uint64_t)s_rows[i] * a.Sp + g0);
-#pragma unroll
-    for (int h = 0; h < E / 4; ++h) {
-      const float4 x = __ldcs(src + h);
-      k[4 * h] = x.x;
-      k[4 * h + 1] = x.y;
-      k[4 * h + 2] = x.z;
-      k[4 * h + 3] = x.w;
-    }
-    loads += E / 4;
-    return true;
-  };
-  float buf[D][E];
-  bool has[D];
-#pragma unroll
-  for (int d = 0; d < D; ++d) has[d] = fetch(d, buf[d]);
-  for (int i0 = 0; i0 < nrows; i0 += D) {
-#pragma unroll
-    for (int d = 0; d < D; ++d) {
-      const int i = i0 + d;
-      if (i >= nrows) break;
-      float k[E];
-#pragma unroll
-      for (int e = 0; e < E; ++e) k[e] = buf[d][e];
-      const bool hk = has[d];
-      has[d] = fetch(i + D, buf[d]);
-      // warp-uniform: no lane of the warp loaded this row -> nothing admissible
-      if (!__any_sync(0xffffffffu, hk)) continue;
-      const int cnt = s_cnt[i], off = s_off[i];
-      for (int q = 0; q < cnt; ++q) {
-        const uint64_t ncp = s_ncp[off + q];
-        if ((winter & ncp) != 0) continue;  // warp-uniform: nothing admissible in the warp
-        // lane maximum; a lane whose sector misses the pair's set contributes nothing,
-        // a lane whose every entry is admissible skips the per-entry tests
-        float mx = -INFINITY;
-        if (hk && (inter & ncp) == 0) {
-          if ((uni & ncp) == 0) {
-#pragma unroll
-            for (int e = 0; e < E; ++e) mx = fmaxf(mx, k[e]);
-          } else {
-#pragma unroll
-            for (int e = 0; e < E; ++e) mx = fmaxf(mx, (m[e] & ncp) == 0 ? k[e] : -INFINITY);
-          }
-        }
-        const uint32_t ko = mx != -INFINITY ? ordkey(mx) : 0u;
-        const uint32_t mxw = __reduce_max_sync(0xffffffffu, ko);
-        unsigned long long* cell = &s_cell[2 * (off + q)];
-        // locate only when the warp can still raise or tie the CTA's cell
-        if (mxw != 0u && mxw >= (uint32_t)(*reinterpret_cast<volatile unsigned long long*>(cell) >> 32)) {
-          uint32_t glast = 0u, gfirst = 0xFFFFFFFFu;
-          if (ko == mxw) {
-            uint32_t bits = 0;
-#pragma unroll
-            for (int e = 0; e < E; ++e) bits |= ((m[e] & ncp) == 0 && k[e] == mx ? 1u : 0u) << e;
-            gfirst = (uint32_t)g0 + (__ffs(bits) - 1);
-            glast = (uint32_t)g0 + (31 - __clz(bits));
-          }
-          const uint32_t ghi = __reduce_max_sync(0xffffffffu, glast);
-          const uint32_t glo = __reduce_min_sync(0xffffffffu, gfirst);
-          if (lane == 0) {
-            atomicMax(cell, ((unsigned long long)mxw << 32) | ghi);
-            atomicMax(cell + 1, ((unsigned long long)mxw << 32) | (uint32_t)~glo);
-          }
-        }
-      }
-    }
-  }
-  __syncthreads();
-  for (int i = warp; i < nrows; i += T / 32) {  // CTA maxima into the global cells
-    const int v = s_rows[i], cnt = s_cnt[i], off = s_off[i];
-    for (int q = lane; q < cnt; q += 32) {
-      const unsigned long long c0 = s_cell[2 * (off + q)], c1 = s_cell[2 * (off + q) + 1];
-      if (c0 != 0ull) {
-        const PairRec pr = a.buckets[(b * n + v) * kMaxChains + q];
-        unsigned long long* cell = a.cell + 2ull * (pr.chain * n + pr.slot);
-        cell_flush(cell, c0);
-        cell_flush(cell + 1, c1);
-      }
-    }
-  }
-  if (a.sector_loads) {
     for (int off = 16; off > 0; off >>= 1) loads += __shfl_down_sync(0xffffffffu, loads, off);
     if (lane == 0 && loads) atomicAdd(a.sector_loads, loads);
   }

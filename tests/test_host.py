@@ -213,3 +213,28 @@ def test_k1_partition_usage_errors():
     assert _lib.lib().bnmc_gpu_k1_partition(c, 10, 5, 9, 2, cuts) == 2
     bad = np.array([3, 1, 3, 3, 3], np.int32)
     assert _lib.lib().bnmc_gpu_k1_partition(bad, 10, 5, 2, 2, cuts) == 3
+
+
+def test_fastdiv_reciprocal_modulo_is_exact():
+    """The walk kernel's propose_swap draws next_below(n) / next_below(n - 1)
+    (rng.hpp:31-38) through FastDiv (common.cuh): q = umulhi(x, floor((2^64-1)/d))
+    is floor(x/d) minus at most 2, so two corrections give x % d exactly. Checked
+    here on the arithmetic for every node-count bound and adversarial x; the GPU
+    chain-trace parity tests check the device code."""
+    rng = np.random.default_rng(5)
+    M = (1 << 64) - 1
+    xs = [int(x) for x in rng.integers(0, 1 << 63, 2000, dtype=np.uint64)] + \
+         [M - i for i in range(64)] + list(range(200))
+    for d in range(2, 65):
+        m = M // d
+        near = [k * d + r for k in (M // d, M // d - 1, 1 << 40) for r in (0, 1, d - 1) if k * d + r <= M]
+        for x in xs + near:
+            q = (x * m) >> 64
+            r = x - q * d
+            assert 0 <= r < 3 * d
+            if r >= d:
+                r -= d
+            if r >= d:
+                r -= d
+            assert r == x % d, (x, d)
+        assert (-d) % (1 << 64) % d == ((1 << 64) - d) % d  # rejection threshold

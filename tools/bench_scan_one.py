@@ -1,7 +1,6 @@
 """Dev: time the K2 order-scan kernel alone (cold L2 per launch):
 python tools/bench_scan_one.py C lo hi reps [cfg]. Prints launch time, key bytes
-streamed per launch and the achieved GB/s. BNMC_SCAN_KERNEL / BNMC_SCAN3 pick
-the variant (see bnmc_gpu.cu scan_geometry)."""
+streamed per launch and the achieved GB/s."""
 import os, sys, ctypes as Cc
 import numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -16,6 +15,5 @@ ms, kb = Cc.c_float(), Cc.c_uint64()
 _lib.check(_lib.lib().bnmc_gpu_bench_scan(cache.handle, perms.ravel(), C, lo, hi, reps, 1,
                                           Cc.byref(ms), Cc.byref(kb)))
 us = ms.value * 1e3
-print(f"kernel={os.environ.get('BNMC_SCAN_KERNEL', '3')} v={os.environ.get('BNMC_SCAN3', '8,4')} "
-      f"C={C} rows {lo}..{hi}: scan {us:.1f} us, {kb.value / 1e6:.1f} MB keys, "
+print(f"C={C} rows {lo}..{hi}: scan {us:.1f} us, {kb.value / 1e6:.1f} MB keys, "
       f"{kb.value / us / 1e3:.0f} GB/s", flush=True)

@@ -4,8 +4,8 @@
 set -u
 D=gpurun_out/san; mkdir -p $D
 CS=/usr/local/cuda/bin/compute-sanitizer
-for tool in memcheck racecheck synccheck; do
-  for c in k1 wide multi walk1 walk8 walk32 spec scan recheck; do
+for tool in ${SAN_TOOLS:-memcheck racecheck synccheck}; do
+  for c in ${SAN_CASES:-k1 wide multi walk1 walk8 walk32 spec scan recheck}; do
     extra=""
     [ $tool = memcheck ] && extra="--leak-check full"
     [ $tool = racecheck ] && extra="--racecheck-report all"
