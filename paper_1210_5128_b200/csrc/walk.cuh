@@ -136,6 +136,23 @@ struct WalkArgs {
   double* out_total;                   // [C]
 };
 
+// mh_accept (sampler.cpp:54-56) on the device: log10(u) < delta for the
+// iteration's next_unit_open() draw u. u lies in [2^-54, 1 - 2^-54], so
+// log10(u) lies in [-16.26, 0): delta >= 0 always accepts and delta < -17
+// always rejects without the logarithm (most proposals at equilibrium). In
+// between, CUDA's log10 may differ from glibc's in the last bits: a decision
+// within tol_rel of the threshold sets *amb and the host replays the chain
+// with glibc thresholds (bnmc_gpu_run_chains).
+template <class Flag>
+__device__ __forceinline__ bool mh_accept_dev(double u, double delta, double tol_rel, Flag* amb) {
+  if (delta >= 0.0) return true;
+  if (delta < -17.0) return false;
+  const double l = log10(u);
+  const double tol = fabs(l) * tol_rel;
+  if (!(l + tol < delta) && !(l - tol >= delta)) *amb = 1;
+  return l < delta;
+}
+
 // a precedes b in the reference enumeration over predecessor positions (sizes
 // descending, then lexicographic on sorted positions). Masks are candidate
 // positions of row v; ppos[node] = position in the current order.
@@ -710,9 +727,10 @@ __global__ void __launch_bounds__(walk_cta_threads<TW>(), TW == 1 ? kWalkMinBloc
           // issued now, consumed after the scan: the load overlaps the pair work
           thr_t = A.thr[(uint64_t)c * (A.iters + 1) + t];
         } else {
-          // mh_accept's draw (sampler.cpp:54-56): one per iteration, split(3)
+          // mh_accept's draw (sampler.cpp:54-56): one per iteration, split(3);
+          // its logarithm only when the decision needs it (mh_accept_dev)
           Rng ar{S.arng};
-          thr_t = log10(ar.next_unit_open());
+          thr_t = ar.next_unit_open();
           S.arng = ar.s;
         }
       }
@@ -735,12 +753,24 @@ __global__ void __launch_bounds__(walk_cta_threads<TW>(), TW == 1 ? kWalkMinBloc
       uint64_t bit[2];
       bool take[2], dl[2];
       const int xnode = S.prop[hi], ynode = S.prop[lo];
+      // the node moved to lo (Y) keeps a subset of its predecessors: a best that
+      // is not an exact tie and whose parents all precede lo stays the unique
+      // maximum, so the row is not rescanned
+      uint64_t below_lo = 0;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int p = 2 * lane + h;
+        if (p < lo) below_lo |= 1ull << S.prop[p];
+      }
+      below_lo = ((uint64_t)__reduce_or_sync(0xffffffffu, (unsigned)(below_lo >> 32)) << 32) |
+                 __reduce_or_sync(0xffffffffu, (unsigned)below_lo);
+      const bool keep_y = !BNMC_FRESH && !((S.tied >> ynode) & 1ull) && (S.cm[ynode] & ~below_lo) == 0;
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int p = 2 * lane + h;
         const int v = p < n ? S.prop[p] : 0;
         bit[h] = p < n ? 1ull << v : 0ull;
-        take[h] = p < n && ((p >= lo && p <= hi) || (p > hi && (S.tied & bit[h])));
+        take[h] = p < n && ((p >= lo && p <= hi && !(p == lo && keep_y)) || (p > hi && (S.tied & bit[h])));
         // middle rows of a swap: the node at hi (X) left the predecessors, the
         // node at lo (Y) joined; delta-eligible when the current best avoids X
         // and is not an exact tie. A walked delta row whose Y-list head (the
@@ -836,16 +866,11 @@ __global__ void __launch_bounds__(walk_cta_threads<TW>(), TW == 1 ? kWalkMinBloc
         atomicCAS(A.stat + 3, 0ull, (unsigned long long)(t - 1));
         atomicExch(A.error, kErrDrift);
       }
-      // mh_accept, sampler.cpp:54-56: log10(u) < new - old
+      // mh_accept, sampler.cpp:54-56: log10(u) < new - old (thr_t = host glibc
+      // log10(u) when A.thr, else u itself)
       const double delta = tot - S.cur_total;
-      bool acc = t == 0 || thr_t < delta;
-      if (!BNMC_FRESH && !A.thr) {
-        // CUDA's log10 and glibc's may differ in the last bits: a decision
-        // within the bound of the threshold is flagged, and the host replays
-        // the chain with glibc thresholds (bnmc_gpu_run_chains).
-        const double tol = fabs(thr_t) * A.accept_tol;
-        if (!(thr_t + tol < delta) && !(thr_t - tol >= delta)) S.amb = 1;
-      }
+      bool acc = true;
+      if (!BNMC_FRESH) acc = A.thr ? thr_t < delta : mh_accept_dev(thr_t, delta, A.accept_tol, &S.amb);
       S.accept = acc;
     }
     team_sync<TW>(team);
@@ -1018,7 +1043,7 @@ __global__ void __launch_bounds__(1024, 1) walk_spec_kernel(WalkArgs A) {
             S.thr = A.thr[(uint64_t)c * (A.iters + 1) + it];
             ar.next_u64();  // keep the device stream in step (unused with host thresholds)
           } else {
-            S.thr = log10(ar.next_unit_open());
+            S.thr = ar.next_unit_open();  // u; its log10 only if needed (mh_accept_dev)
           }
         }
         S.rng_after = pr.s;
@@ -1047,12 +1072,21 @@ __global__ void __launch_bounds__(1024, 1) walk_spec_kernel(WalkArgs A) {
       uint64_t bit[2];
       bool take[2], dl[2];
       const int xnode = S.prop[hi], ynode = S.prop[lo];
+      uint64_t below_lo = 0;  // Y's row keeps an untied best inside its new predecessors
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int p = 2 * lane + h;
+        if (p < lo) below_lo |= 1ull << S.prop[p];
+      }
+      below_lo = ((uint64_t)__reduce_or_sync(0xffffffffu, (unsigned)(below_lo >> 32)) << 32) |
+                 __reduce_or_sync(0xffffffffu, (unsigned)below_lo);
+      const bool keep_y = t > 0 && !((s_tied >> ynode) & 1ull) && (s_cm[ynode] & ~below_lo) == 0;
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int p = 2 * lane + h;
         const int v = p < n ? S.prop[p] : 0;
         bit[h] = p < n ? 1ull << v : 0ull;
-        take[h] = p < n && ((p >= lo && p <= hi) || (p > hi && (s_tied & bit[h])));
+        take[h] = p < n && ((p >= lo && p <= hi && !(p == lo && keep_y)) || (p > hi && (s_tied & bit[h])));
         // delta rows whose Y-list head is below the current best keep it
         // (as in walk_chain_kernel's pair list)
         dl[h] = take[h] && t > 0 && p > lo && p < hi && (p <= A.pe || A.yeff) &&
@@ -1141,11 +1175,8 @@ __global__ void __launch_bounds__(1024, 1) walk_spec_kernel(WalkArgs A) {
       if (n & 1) tot += S.pb[n - 1];
       S.total = tot;
       const double delta = tot - s_cur_total;
-      S.acc = (uint8_t)(it == 0 || S.thr < delta);  // mh_accept, sampler.cpp:54-56
-      if (it > 0 && !A.thr) {
-        const double tol = fabs(S.thr) * A.accept_tol;
-        if (!(S.thr + tol < delta) && !(S.thr - tol >= delta)) S.amb = 1;
-      }
+      // mh_accept, sampler.cpp:54-56 (S.thr: host glibc log10(u) when A.thr, else u)
+      S.acc = (uint8_t)(it == 0 || (A.thr ? S.thr < delta : mh_accept_dev(S.thr, delta, A.accept_tol, &S.amb)));
     }
     __syncthreads();
     // ---- commit in sequence (warp 0) up to and including the first acceptance
