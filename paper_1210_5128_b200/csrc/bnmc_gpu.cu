@@ -245,12 +245,14 @@ struct bnmc_table {
   int last_G = 0;
   // Multi-GPU table (n_gpus > 1): full replicas on the other devices, owned.
   std::vector<bnmc_table*> replicas;
+  cudaStream_t stream2 = nullptr;  // second launch stream of pipelined chain blocks
   ~bnmc_table() {
     for (bnmc_table* r : replicas) {
       cudaSetDevice(r->dev);
       delete r;
     }
     cudaSetDevice(dev);
+    if (stream2) cudaStreamDestroy(stream2);
     if (stream) cudaStreamDestroy(stream);
   }
 };
@@ -746,7 +748,9 @@ void ensure_sorted(bnmc_table* t) {
 // Team size: warps per chain (8 = one chain per CTA, 1 = one chain per warp).
 // 0 = auto: whole-CTA chains while they fill the GPU at 4 CTAs per SM,
 // otherwise one warp per chain.
-void launch_walk(bnmc_table* t, const WalkArgs& A, int C, int team_warps = 0) {
+void launch_walk(bnmc_table* t, const WalkArgs& A, int C, int team_warps = 0,
+                 cudaStream_t st = nullptr) {
+  if (!st) st = t->stream;
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, t->dev);
   int tw = team_warps;
@@ -762,7 +766,7 @@ void launch_walk(bnmc_table* t, const WalkArgs& A, int C, int team_warps = 0) {
   // speculation pays once chains settle (lower acceptance): long runs only
   if (tw == 32 && A.perms == nullptr && !no_spec && A.iters >= 1000 && !A.recheck) {
     // few chains: one 1024-thread CTA per chain evaluating kSpecD proposals per round
-    walk_spec_kernel<<<C, 1024, 0, t->stream>>>(A);
+    walk_spec_kernel<<<C, 1024, 0, st>>>(A);
     CK(cudaGetLastError());
     t->last_team = 32;
     t->last_wu = 8;
@@ -776,9 +780,9 @@ void launch_walk(bnmc_table* t, const WalkArgs& A, int C, int team_warps = 0) {
     const int rcta = std::max(kWalkThreads, 32 * rtw);
     const int rper = rcta / (32 * rtw);
     const unsigned rgrid = static_cast<unsigned>((C + rper - 1) / rper);
-    if (rtw == 32) walk_chain_kernel<32, 8, true><<<rgrid, rcta, 0, t->stream>>>(A);
-    else if (rtw == 8) walk_chain_kernel<8, 8, true><<<rgrid, rcta, 0, t->stream>>>(A);
-    else walk_chain_kernel<1, kWalkUnroll, true><<<rgrid, rcta, 0, t->stream>>>(A);
+    if (rtw == 32) walk_chain_kernel<32, 8, true><<<rgrid, rcta, 0, st>>>(A);
+    else if (rtw == 8) walk_chain_kernel<8, 8, true><<<rgrid, rcta, 0, st>>>(A);
+    else walk_chain_kernel<1, kWalkUnroll, true><<<rgrid, rcta, 0, st>>>(A);
     CK(cudaGetLastError());
     t->last_team = rtw;
     t->last_wu = rtw >= 8 ? 8 : kWalkUnroll;
@@ -786,20 +790,20 @@ void launch_walk(bnmc_table* t, const WalkArgs& A, int C, int team_warps = 0) {
     return;
   }
   switch (tw) {
-    case 32: walk_chain_kernel<32><<<grid, cta, 0, t->stream>>>(A); break;
-    case 16: walk_chain_kernel<16><<<grid, cta, 0, t->stream>>>(A); break;
-    case 8: walk_chain_kernel<8><<<grid, cta, 0, t->stream>>>(A); break;
+    case 32: walk_chain_kernel<32><<<grid, cta, 0, st>>>(A); break;
+    case 16: walk_chain_kernel<16><<<grid, cta, 0, st>>>(A); break;
+    case 8: walk_chain_kernel<8><<<grid, cta, 0, st>>>(A); break;
     case 4:
-      if (deep) walk_chain_kernel<4, 8><<<grid, cta, 0, t->stream>>>(A);
-      else walk_chain_kernel<4><<<grid, cta, 0, t->stream>>>(A);
+      if (deep) walk_chain_kernel<4, 8><<<grid, cta, 0, st>>>(A);
+      else walk_chain_kernel<4><<<grid, cta, 0, st>>>(A);
       break;
     case 2:
-      if (deep) walk_chain_kernel<2, 8><<<grid, cta, 0, t->stream>>>(A);
-      else walk_chain_kernel<2><<<grid, cta, 0, t->stream>>>(A);
+      if (deep) walk_chain_kernel<2, 8><<<grid, cta, 0, st>>>(A);
+      else walk_chain_kernel<2><<<grid, cta, 0, st>>>(A);
       break;
     case 1:
-      if (deep) walk_chain_kernel<1, 8><<<grid, cta, 0, t->stream>>>(A);
-      else walk_chain_kernel<1><<<grid, cta, 0, t->stream>>>(A);
+      if (deep) walk_chain_kernel<1, 8><<<grid, cta, 0, st>>>(A);
+      else walk_chain_kernel<1><<<grid, cta, 0, st>>>(A);
       break;
     default: raise(BNMC_USAGE, "team_warps must be 0, 1, 2, 4, 8, 16 or 32");
   }
@@ -1006,30 +1010,69 @@ void walk_launch(bnmc_table* t, const uint64_t* seeds, int C, const bnmc_chain_p
   A.final_score = t->d_fs.p;
   A.accepted = t->d_acc.p;
   A.recheck = params->debug_recheck != 0;
-  cudaEvent_t e0, e1;
-  CK(cudaEventCreate(&e0));
-  CK(cudaEventCreate(&e1));
-  CK(cudaEventRecord(e0, t->stream));
-  launch_walk(t, A, C, params->team_warps);
-  CK(cudaEventRecord(e1, t->stream));
-  if (trace_proposed)
-    CK(cudaMemcpyAsync(trace_proposed, t->tr_prop.p, 8ull * C * iters, cudaMemcpyDeviceToHost, t->stream));
-  if (trace_accepted)
-    CK(cudaMemcpyAsync(trace_accepted, t->tr_acc.p, 1ull * C * iters, cudaMemcpyDeviceToHost, t->stream));
-  if (trace_best)
-    CK(cudaMemcpyAsync(trace_best, t->tr_best.p, 8ull * C * iters, cudaMemcpyDeviceToHost, t->stream));
-  if (tracker_masks)
-    CK(cudaMemcpyAsync(tracker_masks, t->tmasks.p, 8ull * C * K * n, cudaMemcpyDeviceToHost, t->stream));
-  if (tracker_totals)
-    CK(cudaMemcpyAsync(tracker_totals, t->ttotals.p, 8ull * C * K, cudaMemcpyDeviceToHost, t->stream));
-  if (final_order)
-    CK(cudaMemcpyAsync(final_order, t->d_fo.p, sizeof(int) * C * n, cudaMemcpyDeviceToHost, t->stream));
-  if (final_score)
-    CK(cudaMemcpyAsync(final_score, t->d_fs.p, 8ull * C, cudaMemcpyDeviceToHost, t->stream));
-  if (accepted)
-    CK(cudaMemcpyAsync(accepted, t->d_acc.p, 8ull * C, cudaMemcpyDeviceToHost, t->stream));
-  if (tracker_count)
-    CK(cudaMemcpyAsync(tracker_count, t->d_tc.p, sizeof(int) * C, cudaMemcpyDeviceToHost, t->stream));
+  // Chain blocks: with page-locked result buffers and many chains the chains
+  // run as kBlocks launches alternating over two streams, and each block's
+  // results are copied to the host while the next block computes (its CTAs
+  // fill the SMs as the previous block's retire, so the split costs no tail).
+  // Chains are independent and every result is the reference's bit for bit
+  // whatever the launch split.
+  static const int kBlocks = static_cast<int>(std::max<uint64_t>(1, env_u64("BNMC_CHAIN_BLOCKS", 4)));
+  constexpr int kBlockMinChains = 4096;
+  cudaPointerAttributes pa{};
+  const bool pinned = trace_proposed && cudaPointerGetAttributes(&pa, trace_proposed) == cudaSuccess &&
+                      pa.type == cudaMemoryTypeHost;
+  cudaGetLastError();  // a pageable pointer may leave an error behind on old drivers
+  const int B = pinned && C >= kBlocks * kBlockMinChains && !A.recheck ? kBlocks : 1;
+  if (B > 1 && !t->stream2) CK(cudaStreamCreateWithFlags(&t->stream2, cudaStreamNonBlocking));
+  std::vector<cudaEvent_t> ev(B + 1);
+  for (auto& e : ev) CK(cudaEventCreate(&e));
+  CK(cudaEventRecord(ev[0], t->stream));
+  if (B > 1) CK(cudaStreamWaitEvent(t->stream2, ev[0], 0));
+  for (int b = 0; b < B; ++b) {
+    const int c0 = static_cast<int>(static_cast<int64_t>(C) * b / B);
+    const int c1 = static_cast<int>(static_cast<int64_t>(C) * (b + 1) / B);
+    const int Cb = c1 - c0;
+    const uint64_t o = static_cast<uint64_t>(c0);
+    cudaStream_t st = b % 2 == 0 ? t->stream : t->stream2;
+    WalkArgs Ab = A;
+    Ab.C = Cb;
+    Ab.seeds = A.seeds + o;
+    if (A.thr) Ab.thr = A.thr + o * (iters + 1);
+    Ab.ambiguous = A.ambiguous + o;
+    Ab.tmasks = A.tmasks + o * K * n;
+    Ab.ttotals = A.ttotals + o * K;
+    Ab.thash = A.thash + o * K;
+    Ab.tcount = A.tcount + o;
+    Ab.tr_prop = A.tr_prop + o * iters;
+    Ab.tr_acc = A.tr_acc + o * iters;
+    Ab.tr_best = A.tr_best + o * iters;
+    Ab.final_order = A.final_order + o * n;
+    Ab.final_score = A.final_score + o;
+    Ab.accepted = A.accepted + o;
+    launch_walk(t, Ab, Cb, params->team_warps, st);
+    CK(cudaEventRecord(ev[b + 1], st));
+    auto d2h = [&](auto* dst, const auto* src, uint64_t per) {
+      if (dst)
+        CK(cudaMemcpyAsync(dst + o * per, src + o * per, sizeof(*src) * per * Cb,
+                           cudaMemcpyDeviceToHost, st));
+    };
+    d2h(trace_proposed, t->tr_prop.p, iters);
+    d2h(trace_accepted, t->tr_acc.p, iters);
+    d2h(trace_best, t->tr_best.p, iters);
+    d2h(tracker_masks, t->tmasks.p, static_cast<uint64_t>(K) * n);
+    d2h(tracker_totals, t->ttotals.p, static_cast<uint64_t>(K));
+    d2h(final_order, t->d_fo.p, static_cast<uint64_t>(n));
+    d2h(final_score, t->d_fs.p, 1);
+    d2h(accepted, reinterpret_cast<const uint64_t*>(t->d_acc.p), 1);
+    d2h(tracker_count, t->d_tc.p, 1);
+  }
+  if (B > 1) {  // join: the primary stream waits for the second one
+    cudaEvent_t j;
+    CK(cudaEventCreate(&j));
+    CK(cudaEventRecord(j, t->stream2));
+    CK(cudaStreamWaitEvent(t->stream, j, 0));
+    cudaEventDestroy(j);
+  }
   std::vector<int> amb(C, 0);
   if (!host_thr)
     CK(cudaMemcpyAsync(amb.data(), t->d_amb.p, sizeof(int) * C, cudaMemcpyDeviceToHost, t->stream));
@@ -1037,9 +1080,12 @@ void walk_launch(bnmc_table* t, const uint64_t* seeds, int C, const bnmc_chain_p
   CK(cudaMemcpyAsync(stats, t->stat.p, 32, cudaMemcpyDeviceToHost, t->stream));
   CK(cudaStreamSynchronize(t->stream));
   float ms = 0.f;
-  CK(cudaEventElapsedTime(&ms, e0, e1));
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
+  for (int b = 1; b <= B; ++b) {  // device time: first launch to the last block's end
+    float x = 0.f;
+    CK(cudaEventElapsedTime(&x, ev[0], ev[b]));
+    ms = std::max(ms, x);
+  }
+  for (auto& e : ev) cudaEventDestroy(e);
   if (device_ms) *device_ms = ms;
   if (amb_out) {
     amb_out->clear();

@@ -71,6 +71,10 @@ constexpr uint64_t kWalkCapDiv = 512;
 constexpr uint64_t kDeepRowEntries = 1ull << 21;
 constexpr uint64_t kWalkBudget = BNMC_WALK_BUDGET_DEFAULT;
 constexpr int kXLevels = 3;  // nested exclusion lists per row (strongest parents)
+#ifndef BNMC_LOG_SKIP
+#define BNMC_LOG_SKIP 1
+#endif
+constexpr bool kLogSkip = BNMC_LOG_SKIP;  // A/B switch (tools/build_variant.sh)
 constexpr int kErrDrift = 7;  // error flag: debug_recheck found a drifted chain total
 constexpr uint64_t kRecheckEvery = 100;  // sampler.cpp:105
 
@@ -145,8 +149,10 @@ struct WalkArgs {
 // with glibc thresholds (bnmc_gpu_run_chains).
 template <class Flag>
 __device__ __forceinline__ bool mh_accept_dev(double u, double delta, double tol_rel, Flag* amb) {
-  if (delta >= 0.0) return true;
-  if (delta < -17.0) return false;
+  if (kLogSkip) {
+    if (delta >= 0.0) return true;
+    if (delta < -17.0) return false;
+  }
   const double l = log10(u);
   const double tol = fabs(l) * tol_rel;
   if (!(l + tol < delta) && !(l - tol >= delta)) *amb = 1;
@@ -753,24 +759,12 @@ __global__ void __launch_bounds__(walk_cta_threads<TW>(), TW == 1 ? kWalkMinBloc
       uint64_t bit[2];
       bool take[2], dl[2];
       const int xnode = S.prop[hi], ynode = S.prop[lo];
-      // the node moved to lo (Y) keeps a subset of its predecessors: a best that
-      // is not an exact tie and whose parents all precede lo stays the unique
-      // maximum, so the row is not rescanned
-      uint64_t below_lo = 0;
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int p = 2 * lane + h;
-        if (p < lo) below_lo |= 1ull << S.prop[p];
-      }
-      below_lo = ((uint64_t)__reduce_or_sync(0xffffffffu, (unsigned)(below_lo >> 32)) << 32) |
-                 __reduce_or_sync(0xffffffffu, (unsigned)below_lo);
-      const bool keep_y = !BNMC_FRESH && !((S.tied >> ynode) & 1ull) && (S.cm[ynode] & ~below_lo) == 0;
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int p = 2 * lane + h;
         const int v = p < n ? S.prop[p] : 0;
         bit[h] = p < n ? 1ull << v : 0ull;
-        take[h] = p < n && ((p >= lo && p <= hi && !(p == lo && keep_y)) || (p > hi && (S.tied & bit[h])));
+        take[h] = p < n && ((p >= lo && p <= hi) || (p > hi && (S.tied & bit[h])));
         // middle rows of a swap: the node at hi (X) left the predecessors, the
         // node at lo (Y) joined; delta-eligible when the current best avoids X
         // and is not an exact tie. A walked delta row whose Y-list head (the
@@ -1072,21 +1066,12 @@ __global__ void __launch_bounds__(1024, 1) walk_spec_kernel(WalkArgs A) {
       uint64_t bit[2];
       bool take[2], dl[2];
       const int xnode = S.prop[hi], ynode = S.prop[lo];
-      uint64_t below_lo = 0;  // Y's row keeps an untied best inside its new predecessors
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int p = 2 * lane + h;
-        if (p < lo) below_lo |= 1ull << S.prop[p];
-      }
-      below_lo = ((uint64_t)__reduce_or_sync(0xffffffffu, (unsigned)(below_lo >> 32)) << 32) |
-                 __reduce_or_sync(0xffffffffu, (unsigned)below_lo);
-      const bool keep_y = t > 0 && !((s_tied >> ynode) & 1ull) && (s_cm[ynode] & ~below_lo) == 0;
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int p = 2 * lane + h;
         const int v = p < n ? S.prop[p] : 0;
         bit[h] = p < n ? 1ull << v : 0ull;
-        take[h] = p < n && ((p >= lo && p <= hi && !(p == lo && keep_y)) || (p > hi && (s_tied & bit[h])));
+        take[h] = p < n && ((p >= lo && p <= hi) || (p > hi && (s_tied & bit[h])));
         // delta rows whose Y-list head is below the current best keep it
         // (as in walk_chain_kernel's pair list)
         dl[h] = take[h] && t > 0 && p > lo && p < hi && (p <= A.pe || A.yeff) &&

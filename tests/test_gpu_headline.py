@@ -149,3 +149,29 @@ def test_walk_cap_retune_rebuilds_pst():
     t = port.cache_build(data.cells, data.cards, cfg.max_parents)
     o = port.run_mcmc(t, cfg.max_parents, 300, 1, pri)
     np.testing.assert_array_equal(a[0].trace_proposed, o["trace_proposed"])
+
+
+def test_pipelined_chain_blocks_equal_single_launch(cfg4):
+    """>= 16,384 chains with page-locked result buffers run as chain blocks on
+    two streams with overlapped result copies (walk_launch); pageable buffers
+    take the single launch. Both must give the same bytes, chain by chain, and
+    sampled chains equal the plain-C oracle."""
+    data, pri, cfg, cache = cfg4
+    c = P.RunConfig(max_parents=cfg.max_parents, iterations=40, track_top=cfg.track_top,
+                    memory_cap_bytes=cfg.memory_cap_bytes)
+    seeds = np.arange(1, 16385, dtype=np.uint64)
+    n = data.n
+    pinned = P.run_chains_batch(cache, pri, seeds, c)  # pooled page-locked buffers
+    pageable = P.run_chains_batch(cache, pri, seeds, c,
+                                  P.api.ChainBatch.allocate(seeds.size, 40, n, c.track_top,
+                                                            pinned=False))
+    for f in ("trace_proposed", "trace_accepted", "trace_best", "final_order", "final_score",
+              "accepted", "tracker_count", "tracker_masks", "tracker_totals"):
+        np.testing.assert_array_equal(np.asarray(getattr(pinned, f)).view(np.uint8),
+                                      np.asarray(getattr(pageable, f)).view(np.uint8), err_msg=f)
+    if not ref.available():
+        return
+    rc = ref_cache_of(cache, cfg)
+    for ci in (0, 4095, 4096, 8191, 12288, 16383):  # both sides of every block edge
+        r = ref_chain(rc, n, cfg.max_parents, 40, int(seeds[ci]), pri)
+        assert_chain_equal(pinned.result(ci), r, f"chain {ci}")

@@ -1,5 +1,14 @@
-mkdir -p gpurun_out/ab
-timeout 600 python tools/walk_probe.py cfg4 500 18944 > gpurun_out/ab/probe.log 2>&1
-timeout 900 python -m pytest tests/test_gpu_headline.py tests/test_gpu_parity.py tests/test_gpu_edge.py -q -x > gpurun_out/ab/pytest.log 2>&1; echo rc=$? >> gpurun_out/ab/pytest.log
-timeout 600 python bench.py --force-dist --steps 2 --warmup 1 --no-extras --no-cpu-baseline --parity-chains 0 > gpurun_out/ab/dist.json 2> gpurun_out/ab/dist.err
-cat gpurun_out/ab/probe.log; tail -2 gpurun_out/ab/pytest.log; head -c 400 gpurun_out/ab/dist.json; tail -3 gpurun_out/ab/dist.err
+#!/bin/bash
+# Same-box A/B of walk-kernel builds (tools/build_variant.sh) and settings:
+# interleaved walk_probe runs at the bench configuration.
+#   bash tools/walk_ab.sh OUT SPEC...   SPEC = VARIANT[:ENV=VALUE[,ENV=VALUE]]
+set -u
+OUT=gpurun_out/$1; shift; mkdir -p $OUT
+for rep in 1 2 3; do
+  for spec in "$@"; do
+    v=${spec%%:*}; envs=""; [ "$spec" != "$v" ] && envs=$(echo "${spec#*:}" | tr ',' ' ')
+    echo "== $spec rep $rep" >> $OUT/ab.txt
+    env $envs BNMC_B200_LIB=variants/$v/libbnmc_b200.so timeout 300 python tools/walk_probe.py ${CFG:-cfg4} ${ITERS:-500} ${CHAINS:-18944} >> $OUT/ab.txt 2>&1
+  done
+done
+echo done
