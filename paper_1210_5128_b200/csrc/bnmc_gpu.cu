@@ -228,6 +228,8 @@ struct bnmc_table {
   DevBuf<uint64_t> tmasks;
   DevBuf<double> ttotals;
   DevBuf<uint64_t> thash;
+  DevBuf<uint64_t> smasks, shash;  // slot tracker storage (track_top <= kTrackSlots)
+  DevBuf<double> stotals;
   DevBuf<double> tr_prop, tr_best;
   DevBuf<uint8_t> tr_acc;
   DevBuf<unsigned long long> stat;
@@ -975,6 +977,12 @@ void walk_launch(bnmc_table* t, const uint64_t* seeds, int C, const bnmc_chain_p
   t->tmasks.alloc(static_cast<size_t>(C) * K * n);
   t->ttotals.alloc(static_cast<size_t>(C) * K);
   t->thash.alloc(static_cast<size_t>(C) * K);
+  const bool slots = K <= kTrackSlots;  // slot tracker (walk.cuh tracker_insert_slots)
+  if (slots) {
+    t->smasks.alloc(static_cast<size_t>(C) * K * n);
+    t->stotals.alloc(static_cast<size_t>(C) * K);
+    t->shash.alloc(static_cast<size_t>(C) * K);
+  }
   t->tr_prop.alloc(static_cast<size_t>(C) * iters);
   t->tr_best.alloc(static_cast<size_t>(C) * iters);
   t->tr_acc.alloc(static_cast<size_t>(C) * iters);
@@ -1003,6 +1011,9 @@ void walk_launch(bnmc_table* t, const uint64_t* seeds, int C, const bnmc_chain_p
   A.ttotals = t->ttotals.p;
   A.thash = t->thash.p;
   A.tcount = t->d_tc.p;
+  A.smasks = slots ? t->smasks.p : nullptr;
+  A.stotals = slots ? t->stotals.p : nullptr;
+  A.shash = slots ? t->shash.p : nullptr;
   A.tr_prop = t->tr_prop.p;
   A.tr_acc = t->tr_acc.p;
   A.tr_best = t->tr_best.p;
@@ -1043,6 +1054,11 @@ void walk_launch(bnmc_table* t, const uint64_t* seeds, int C, const bnmc_chain_p
     Ab.ttotals = A.ttotals + o * K;
     Ab.thash = A.thash + o * K;
     Ab.tcount = A.tcount + o;
+    if (slots) {
+      Ab.smasks = A.smasks + o * K * n;
+      Ab.stotals = A.stotals + o * K;
+      Ab.shash = A.shash + o * K;
+    }
     Ab.tr_prop = A.tr_prop + o * iters;
     Ab.tr_acc = A.tr_acc + o * iters;
     Ab.tr_best = A.tr_best + o * iters;

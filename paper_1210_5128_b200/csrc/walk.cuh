@@ -70,7 +70,10 @@ constexpr uint64_t kWalkCapDiv = 512;
 // 13.4M vs 9.0M it/s), shorter rows 4 (cfg4: 100M vs 91M it/s).
 constexpr uint64_t kDeepRowEntries = 1ull << 21;
 constexpr uint64_t kWalkBudget = BNMC_WALK_BUDGET_DEFAULT;
-constexpr int kXLevels = 3;  // nested exclusion lists per row (strongest parents)
+#ifndef BNMC_XLEVELS
+#define BNMC_XLEVELS 6
+#endif
+constexpr int kXLevels = BNMC_XLEVELS;  // nested exclusion lists per row (strongest parents)
 #ifndef BNMC_LOG_SKIP
 #define BNMC_LOG_SKIP 1
 #endif
@@ -123,6 +126,9 @@ struct WalkArgs {
   double* ttotals;                     // [C][K]
   uint64_t* thash;                     // [C][K] graph hashes of the tracker entries
   int* tcount;                         // [C]
+  uint64_t* smasks;                    // [C][K][n] tracker slots (K <= kTrackSlots), or null:
+  double* stotals;                     //   entries unsorted, their order as slot indices in
+  uint64_t* shash;                     //   shared memory; sorted into tmasks/ttotals at exit
   double* tr_prop;                     // [C][iters]
   uint8_t* tr_acc;
   double* tr_best;
@@ -589,6 +595,73 @@ __device__ __noinline__ void tracker_insert_warp(uint64_t* tm, double* tt, uint6
   __syncwarp();
 }
 
+constexpr int kTrackSlots = 32;  // largest track_top served by the slot tracker
+
+// BestGraphTracker::update (sampler.cpp:32-41) with the entries in unsorted
+// slots (tm/tt/th) and their order as slot indices in shared memory (ord): an
+// insertion writes one slot and shifts at most K one-byte indices, instead of
+// moving every lower entry's n masks one place down in global memory. Same
+// dedupe (graph equality, hash first), same lower bound on (total desc, Dag
+// operator<); K <= kTrackSlots, so one ballot covers every entry.
+__device__ __noinline__ void tracker_insert_slots(uint64_t* tm, double* tt, uint64_t* th, int K, int n,
+                                                  const uint64_t* pm, double proposed, int* tcount,
+                                                  uint8_t* ord, double* tmin, double* tbest) {
+  const int lane = threadIdx.x & 31;
+  const int count = *tcount;
+  const bool full = count == K;
+  uint64_t hv = 0;
+  BNMC_FOR_NODES(i, lane, 32, n) hv ^= Rng::mix(pm[i] + 0x9E3779B97F4A7C15ull * (uint64_t)(i + 1));
+  const uint64_t h = ((uint64_t)__reduce_xor_sync(0xffffffffu, (unsigned)(hv >> 32)) << 32) |
+                     __reduce_xor_sync(0xffffffffu, (unsigned)hv);
+  unsigned cand = __ballot_sync(0xffffffffu, lane < count && th[lane] == h);  // slots, any order
+  while (cand) {
+    const int e = __ffs(cand) - 1;
+    cand &= cand - 1;
+    bool eq = true;
+    BNMC_FOR_NODES(i, lane, 32, n) eq &= tm[(uint64_t)e * n + i] == pm[i];
+    if (__all_sync(0xffffffffu, eq)) return;  // already tracked
+  }
+  bool prec = false;  // the lane-th best entry precedes the proposal
+  uint8_t sl = 0;
+  if (lane < count) {
+    sl = ord[lane];
+    const double et = tt[sl];
+    if (et != proposed) {
+      prec = et > proposed;
+    } else {
+      for (int i = 0; i < n; ++i) {
+        const uint64_t x = tm[(uint64_t)sl * n + i], y = pm[i];
+        if (x != y) {
+          prec = x < y;
+          break;
+        }
+      }
+    }
+  }
+  const int ins = __popc(__ballot_sync(0xffffffffu, prec));
+  const int last = full ? count - 1 : count;
+  const int evict = __shfl_sync(0xffffffffu, (int)sl, K - 1);
+  const int slot = full ? evict : count;  // the minimum's slot is reused when full
+  const int prev = __shfl_up_sync(0xffffffffu, (int)sl, 1);
+  __syncwarp();
+  if (lane > ins && lane <= last) ord[lane] = (uint8_t)prev;  // entries [ins, last) move down
+  if (lane == ins) ord[ins] = (uint8_t)slot;
+  BNMC_FOR_NODES(i, lane, 32, n) tm[(uint64_t)slot * n + i] = pm[i];
+  if (lane == 0) {
+    tt[slot] = proposed;
+    th[slot] = h;
+    const int cnt = full ? count : count + 1;
+    *tcount = cnt;
+  }
+  __syncwarp();
+  if (lane == 0) {
+    const int cnt = *tcount;
+    *tbest = tt[ord[0]];
+    *tmin = cnt == K ? tt[ord[K - 1]] : -INFINITY;
+  }
+  __syncwarp();
+}
+
 // kCache: tcache (shared) holds [0] the tracker best and [1] its minimum when
 // full (else -inf), kept current by the insert so the common rejection needs
 // no global load (single-chain kernel); otherwise the tracker is read directly.
@@ -635,6 +708,8 @@ struct TeamState {
   uint64_t tied, tied_new, rng, arng;
   double total, cur_total;
   double tmin;  // tracker minimum when full (-inf before), kept by the insert path
+  double tbest;                    // tracker maximum (slot tracker: trace rows)
+  uint8_t tord[32];                // slot tracker: slot of the e-th best entry
   unsigned long long acc;
   int np, a, b, accept, tcount, amb;
 };
@@ -663,6 +738,7 @@ __device__ __noinline__ void init_team_state(TeamState& S, const WalkArgs& A, in
   S.amb = 0;
   S.tcount = 0;
   S.tmin = -INFINITY;
+  S.tbest = -INFINITY;
   S.acc = 0;
   S.cur_total = 0.0;
 }
@@ -887,10 +963,16 @@ __global__ void __launch_bounds__(walk_cta_threads<TW>(), TW == 1 ? kWalkMinBloc
     // rejection needs no global load)
     if (twarp == 0 && (t == 0 || accepted || !A.strict) && !(S.tcount == A.K && proposed <= S.tmin)) {
       double* tt = A.ttotals + (uint64_t)c * A.K;
-      tracker_insert_warp<false>(A.tmasks + (uint64_t)c * A.K * n, tt, A.thash + (uint64_t)c * A.K, A.K,
-                                 n, S.pm, proposed, &S.tcount, nullptr);
-      __syncwarp();
-      if (lane == 0 && S.tcount == A.K) S.tmin = tt[A.K - 1];
+      if (A.smasks) {
+        const uint64_t so = (uint64_t)c * A.K;
+        tracker_insert_slots(A.smasks + so * n, A.stotals + so, A.shash + so, A.K, n, S.pm, proposed,
+                             &S.tcount, S.tord, &S.tmin, &S.tbest);
+      } else {
+        tracker_insert_warp<false>(A.tmasks + (uint64_t)c * A.K * n, tt, A.thash + (uint64_t)c * A.K,
+                                   A.K, n, S.pm, proposed, &S.tcount, nullptr);
+        __syncwarp();
+        if (lane == 0 && S.tcount == A.K) S.tmin = tt[A.K - 1];
+      }
     }
     // ---- commit + trace row
     if (accepted)
@@ -909,7 +991,7 @@ __global__ void __launch_bounds__(walk_cta_threads<TW>(), TW == 1 ? kWalkMinBloc
         const uint64_t o = (uint64_t)c * A.iters + (t - 1);
         A.tr_prop[o] = proposed;
         A.tr_acc[o] = accepted ? 1 : 0;
-        A.tr_best[o] = A.ttotals[(uint64_t)c * A.K];
+        A.tr_best[o] = A.smasks ? S.tbest : A.ttotals[(uint64_t)c * A.K];
       }
     }
     team_sync<TW>(team);
@@ -919,6 +1001,14 @@ __global__ void __launch_bounds__(walk_cta_threads<TW>(), TW == 1 ? kWalkMinBloc
 #undef BNMC_FRESH
   if (!score_only) {
     BNMC_FOR_NODES(i, ttid, TW * 32, n) A.final_order[(uint64_t)c * n + i] = S.order[i];
+    if (A.smasks && twarp == 0) {  // slot tracker -> tmasks/ttotals in (total desc, Dag <) order
+      const uint64_t so = (uint64_t)c * A.K;
+      for (int e = 0; e < S.tcount; ++e) {
+        const uint64_t sl = S.tord[e];
+        BNMC_FOR_NODES(i, lane, 32, n) A.tmasks[(so + e) * n + i] = A.smasks[(so + sl) * n + i];
+        if (lane == 0) A.ttotals[so + e] = A.stotals[so + sl];
+      }
+    }
     if (ttid == 0) {
       A.final_score[c] = S.cur_total;
       A.accepted[c] = S.acc;
