@@ -241,9 +241,13 @@ def walk_roofline(prof, avg_launch_s, peak, peak_src, alg_bytes, chain_iters_per
     DRAM bytes per launch (ncu capture of this configuration) over this run's
     launch time against the HBM peak; `issue` carries the ncu instruction
     count, IPC and issue-slot use that do bound it."""
-    dram = prof.get("dram_bytes_per_launch")
+    # ncu figures are per chain-iteration of the captured launch (one chain
+    # block), scaled to this step's chain-iterations
+    dpc = prof.get("dram_bytes_per_chain_iteration")
+    dram = dpc * chain_iters_per_launch if dpc else None
     ach = dram / avg_launch_s / 1e9 if dram else None
-    inst = prof.get("warp_instructions")
+    ipc_ = prof.get("warp_instructions_per_chain_iteration")
+    inst = ipc_ * chain_iters_per_launch if ipc_ else None
     return {"bound": "issue/L2 (latency)", "achieved": ach, "peak": peak, "unit": "GB/s",
             "frac": ach / peak if ach else None, "traffic": dram,
             "traffic_source": prof.get("source"),
@@ -394,7 +398,7 @@ def run_ours(args):
         tdist.barrier()
         comm.max([0.0])  # NCCL rendezvous before the timed region
     torch.cuda.synchronize()
-    dev_ms, wall_s, walked, enumerated, pairs, replayed = [], [], 0, 0, 0, 0
+    dev_ms, wall_s, walked, enumerated, pairs, replayed, launches = [], [], 0, 0, 0, 0, 0
     with ClockSampler(local) as clocks:
         for k in range(args.steps):
             flush_l2(torch, flush)
@@ -405,8 +409,11 @@ def run_ours(args):
             pa, wa, en, so = C.c_uint64(), C.c_uint64(), C.c_uint64(), C.c_float()
             _lib.check(_lib.lib().bnmc_gpu_last_walk_stats(cache.handle, C.byref(pa), C.byref(wa),
                                                             C.byref(en), C.byref(so)))
-            rp = C.c_uint64()
+            rp, nl = C.c_uint64(), C.c_uint64()
             _lib.check(_lib.lib().bnmc_gpu_last_replayed(cache.handle, C.byref(rp)))
+            _lib.check(_lib.lib().bnmc_gpu_last_scan_stats(cache.handle, None, None, None,
+                                                            C.byref(nl)))
+            launches += nl.value  # kernel launches the library made for this call
             pairs += pa.value
             walked += wa.value
             enumerated += en.value
@@ -488,7 +495,7 @@ def run_ours(args):
                      "enumerated_per_pair": enumerated / max(1, pairs),
                      "chains_replayed_exact": replayed},
             "precompute_s": pre_s, "precompute_kernel_ms": k1_ms, "fold_ms": fold.value,
-            "gpu_launches": int(args.steps * (1 + (1 if replayed else 0))),
+            "gpu_launches": int(launches),
             "best_total": best["best_total"], "best_chain_seed": best["seed"],
             "cpu_baseline": cpu,
             "clocks": clocks.summary(),

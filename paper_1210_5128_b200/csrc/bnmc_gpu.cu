@@ -1113,7 +1113,7 @@ void walk_launch(bnmc_table* t, const uint64_t* seeds, int C, const bnmc_chain_p
   t->last_sectors = stats[1] + stats[2];  // walk path: entries visited (walked + enumerated)
   t->last_walked = stats[1];
   t->last_enumerated = stats[2];
-  t->last_launches = 1;
+  t->last_launches = B;
   t->last_total_ms = ms;
   t->last_scan_ms = ms;
   t->last_scan_samples = 1;
@@ -1136,6 +1136,7 @@ void run_chains_walk(bnmc_table* t, const uint64_t* seeds, int C, const bnmc_cha
               device_ms, &amb);
   const uint64_t keep[4] = {t->last_rescans, t->last_walked, t->last_enumerated, t->last_sectors};
   const float keep_ms = t->last_scan_ms;
+  const uint64_t keep_launches = t->last_launches;
   t->last_replayed = amb.size();
   if (amb.empty()) return;
   const int R = static_cast<int>(amb.size()), n = t->n, K = params->track_top;
@@ -1169,7 +1170,7 @@ void run_chains_walk(bnmc_table* t, const uint64_t* seeds, int C, const bnmc_cha
   t->last_enumerated = keep[2];
   t->last_sectors = keep[3];
   t->last_scan_ms = keep_ms + replay_ms;
-  t->last_launches = 2;
+  t->last_launches = keep_launches + t->last_launches;
 }
 
 void validate_cards(const int* cards, int n) {

@@ -1066,6 +1066,7 @@ __global__ void __launch_bounds__(1024, 1) walk_spec_kernel(WalkArgs A) {
   __shared__ unsigned long long s_acc;
   __shared__ int s_tcount, s_amb, s_d, s_npairs, s_done_to;
   __shared__ double s_tcache[2];
+  __shared__ uint8_t s_tord[kTrackSlots];  // slot tracker order (A.smasks)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int c = blockIdx.x;
   const int n = A.n;
@@ -1267,9 +1268,15 @@ __global__ void __launch_bounds__(1024, 1) walk_spec_kernel(WalkArgs A) {
         const uint64_t it = t + i;
         const bool acc = S.acc != 0;
         if (lane == 0 && S.amb) s_amb = 1;
-        if (it == 0 || acc || !A.strict)
-          tracker_offer_warp<true>(A.tmasks + (uint64_t)c * A.K * n, A.ttotals + (uint64_t)c * A.K,
-                                   A.thash + (uint64_t)c * A.K, A.K, n, S.pm, S.total, &s_tcount, s_tcache);
+        if (it == 0 || acc || !A.strict) {
+          const uint64_t so = (uint64_t)c * A.K;
+          if (!A.smasks)
+            tracker_offer_warp<true>(A.tmasks + so * n, A.ttotals + so, A.thash + so, A.K, n, S.pm, S.total,
+                                     &s_tcount, s_tcache);
+          else if (!(s_tcount == A.K && S.total <= s_tcache[1]))
+            tracker_insert_slots(A.smasks + so * n, A.stotals + so, A.shash + so, A.K, n, S.pm, S.total,
+                                 &s_tcount, s_tord, &s_tcache[1], &s_tcache[0]);
+        }
         if (lane == 0 && it > 0) {
           const uint64_t o = (uint64_t)c * A.iters + (it - 1);
           A.tr_prop[o] = S.total;
@@ -1306,6 +1313,14 @@ __global__ void __launch_bounds__(1024, 1) walk_spec_kernel(WalkArgs A) {
     t += s_done_to;
   }
   if (tid < n) A.final_order[(uint64_t)c * n + tid] = s_order[tid];
+  if (A.smasks && warp == 0) {  // slot tracker -> tmasks/ttotals in order
+    const uint64_t so = (uint64_t)c * A.K;
+    for (int e = 0; e < s_tcount; ++e) {
+      const uint64_t sl = s_tord[e];
+      BNMC_FOR_NODES(i, lane, 32, n) A.tmasks[(so + e) * n + i] = A.smasks[(so + sl) * n + i];
+      if (lane == 0) A.ttotals[so + e] = A.stotals[so + sl];
+    }
+  }
   if (tid == 0) {
     A.final_score[c] = s_cur_total;
     A.accepted[c] = s_acc;

@@ -1,8 +1,11 @@
 """Write profiles/ncu_traffic.json — the ncu --set full figures of the walk
 kernel at the bench configuration that bench.py reports beside its own timing:
-DRAM bytes, warp instructions, IPC, issue-slot use, top stalls per launch.
-  python tools/ncu_traffic.py REPORT.ncu-rep SUMMARY_NAME
-(SUMMARY_NAME: the profiles/ text summary written by tools/ncu_summary.py)."""
+DRAM bytes, warp instructions, IPC, issue-slot use, top stalls; per launch and per
+chain-iteration of the captured launch (the bench scales the latter to its step:
+the library splits large calls into chain blocks, so a launch is one block).
+  python tools/ncu_traffic.py REPORT.ncu-rep SUMMARY_NAME CHAINS ITERATIONS
+(SUMMARY_NAME: the profiles/ text summary written by tools/ncu_summary.py;
+CHAINS x ITERATIONS: the captured launch's chain-iterations)."""
 import csv
 import io
 import json
@@ -12,6 +15,7 @@ import sys
 
 rep = sys.argv[1]
 summary = sys.argv[2] if len(sys.argv) > 2 else "?"
+chain_iters = int(sys.argv[3]) * int(sys.argv[4]) if len(sys.argv) > 4 else None
 raw = list(csv.reader(io.StringIO(subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"],
                                                  capture_output=True, text=True).stdout)))
 h, u, v = raw[0], raw[1], raw[2]
@@ -47,8 +51,12 @@ out = {"walk_chain_kernel": {
     "issue_slots_busy": (opt("sm__instruction_throughput.avg.pct_of_peak_sustained_active") or 0)
     / 100.0,
     "top_stalls": {k: round(x / tot, 3) for x, k in sorted(st, reverse=True)[:5]},
-    "source": f"ncu --set full --clock-control none of one walk_chain_kernel launch of "
-              f"bench.py --steps 1 (bench configuration): profiles/{summary}"}}
+    "chain_iterations_per_launch": chain_iters,
+    "dram_bytes_per_chain_iteration": (rd + wr) / chain_iters if chain_iters else None,
+    "warp_instructions_per_chain_iteration":
+        (opt("smsp__inst_executed.sum") or 0) / chain_iters if chain_iters else None,
+    "source": f"ncu --set full --clock-control none of one walk_chain_kernel launch (one "
+              f"chain block of the bench step) of bench.py --steps 1: profiles/{summary}"}}
 with open(os.path.join(root, "profiles", "ncu_traffic.json"), "w") as f:
     json.dump(out, f, indent=1)
 print(json.dumps(out, indent=1))
