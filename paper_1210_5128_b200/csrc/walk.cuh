@@ -386,6 +386,34 @@ __device__ __forceinline__ PairOut enum_pst(const WalkArgs& A, int v, const uint
   return r;
 }
 
+// Per-CTA shared-memory copies of the small read-only tables a pair consults:
+// binomials and global_index size-class offsets, PST offsets (the walk cap and
+// the enumeration ranges) and the rows' strongest-parent bits (exclusion
+// levels) — shared loads instead of dependent global ones on every pair.
+struct WalkSm {
+  const uint64_t* bt;     // [65 * 9] binomials
+  const uint64_t* boff;   // [9] global_index size-class offsets (c = n - 1)
+  const uint32_t* poff;   // pst_off [pc + 2]
+  const uint32_t* poff2;  // pst2_off [pe + 1]
+  const uint64_t* xbit;   // [n][kXLevels]
+};
+constexpr int kPoffMax = kMaxNodes + 2;
+
+// Fill the WalkSm tables (every thread of the CTA; a barrier must follow).
+__device__ __forceinline__ void walk_sm_fill(const WalkArgs& A, uint64_t* bt, uint64_t* boff, uint32_t* poff,
+                                             uint32_t* poff2, uint64_t* xbit, int tid, int nthreads) {
+  for (int i = tid; i < 65 * 9; i += nthreads) bt[i] = binom(i / 9, i % 9);
+  if (tid < 9) {
+    uint64_t o = 0;
+    for (int j = tid + 1; j <= A.s; ++j) o += binom(A.n - 1, j);
+    boff[tid] = o;
+  }
+  for (int i = tid; i < A.pc + 2; i += nthreads) poff[i] = A.pst_off[i];
+  for (int i = tid; i < A.pe + 1; i += nthreads) poff2[i] = A.pst2_off[i];
+  if (A.xeff)
+    for (int i = tid; i < A.n * kXLevels; i += nthreads) xbit[i] = A.xbit[i];
+}
+
 // Row of a node whose predecessor set changed from P to P - {X} + {Y}, whose
 // current best (old_eff, old_cm) does not contain X and is not an exact tie:
 // the best over P' is the better of the old best and the best set containing
@@ -403,8 +431,7 @@ struct DeltaIn {
 // = pos of the order being scored; bt = binomial table in shared memory.
 template <int EU, int WU>
 __device__ PairOut pair_argmax(const WalkArgs& A, int v, int p, uint64_t cpred, const uint8_t* order,
-                               const uint8_t* ppos, const uint64_t* bt, const uint64_t* boff,
-                               const DeltaIn& d) {
+                               const uint8_t* ppos, const WalkSm& sm, const DeltaIn& d) {
   const int lane = threadIdx.x & 31;
   PairOut r;
   uint32_t walked_n = 0;
@@ -423,7 +450,7 @@ __device__ PairOut pair_argmax(const WalkArgs& A, int v, int p, uint64_t cpred, 
       r.tied = 0;
       // the list's head is the best set containing Y (admissible or not):
       // below the current best, nothing containing Y can change the row
-      if (__ldg(ye) < d.old_eff) return r;
+      // (the pair list already dropped rows whose list head is below their best)
       WalkHit h;
       bool done = false;
       uint32_t base = 0;
@@ -453,7 +480,7 @@ __device__ PairOut pair_argmax(const WalkArgs& A, int v, int p, uint64_t cpred, 
     // list (same admissible entries in the same order, the others skipped).
     int xj = 0;  // leading strongest parents missing from the predecessors
     if (A.xeff)
-      while (xj < A.xlev && (ncp & __ldg(A.xbit + v * kXLevels + xj))) ++xj;
+      while (xj < A.xlev && (ncp & sm.xbit[v * kXLevels + xj])) ++xj;
     const double* re;
     const uint64_t* rc;
     uint32_t S;
@@ -469,7 +496,7 @@ __device__ PairOut pair_argmax(const WalkArgs& A, int v, int p, uint64_t cpred, 
       S = A.S32;
     }
     const uint32_t lim =
-        p <= A.pc ? (uint32_t)min((uint64_t)S, (uint64_t)A.wbud * (A.pst_off[p + 1] - A.pst_off[p])) : S;
+        p <= A.pc ? (uint32_t)min((uint64_t)S, (uint64_t)A.wbud * (sm.poff[p + 1] - sm.poff[p])) : S;
     WalkHit h;
     // Rounds grow 32, 64, 128, then 32 * WU entries: most first admissible
     // entries sit in the first 32, deep walks still get WU loads per lane in flight.
@@ -507,9 +534,9 @@ __device__ PairOut pair_argmax(const WalkArgs& A, int v, int p, uint64_t cpred, 
   // (PST(p-1, s-1) with Y's position inserted); otherwise every admissible set
   // (PST(p, s)), also after a walk that ran out of budget.
   const bool de = d.on && p <= A.pe;
-  const uint64_t* pst = de ? A.pst2 + A.pst2_off[p - 1] : A.pst + A.pst_off[p];
-  const uint32_t cnt = de ? A.pst2_off[p] - A.pst2_off[p - 1] : A.pst_off[p + 1] - A.pst_off[p];
-  r = enum_pst<EU>(A, v, pst, cnt, de ? d.ypos : -1, order, bt, boff);
+  const uint64_t* pst = de ? A.pst2 + sm.poff2[p - 1] : A.pst + sm.poff[p];
+  const uint32_t cnt = de ? sm.poff2[p] - sm.poff2[p - 1] : sm.poff[p + 1] - sm.poff[p];
+  r = enum_pst<EU>(A, v, pst, cnt, de ? d.ypos : -1, order, sm.bt, sm.boff);
   r.nw = walked_n;
   r.ne = cnt;
   if (de) {
@@ -766,17 +793,15 @@ __global__ void __launch_bounds__(walk_cta_threads<TW>(), TW == 1 ? kWalkMinBloc
   __shared__ uint64_t s_boff[9];  // size-class offsets of global_index for c = n - 1
   __shared__ TeamState s_team[kTeams];
   __shared__ FastDiv s_div[2];  // propose_swap's bounds n and n - 1
+  __shared__ uint32_t s_poff[kPoffMax], s_poff2[kPoffMax];
+  __shared__ uint64_t s_xbit[kMaxNodes * kXLevels];
   const int tid = threadIdx.x, lane = tid & 31;
   const int team = (tid >> 5) / TW, twarp = (tid >> 5) % TW, ttid = tid - team * TW * 32;
   const int c = blockIdx.x * kTeams + team;
   const int n = A.n;
   if (tid < 2) s_div[tid] = FastDiv::make((uint64_t)(n - tid));
-  for (int i = tid; i < 65 * 9; i += kCta) s_bt[i] = binom(i / 9, i % 9);
-  if (tid < 9) {
-    uint64_t o = 0;
-    for (int j = tid + 1; j <= A.s; ++j) o += binom(A.n - 1, j);
-    s_boff[tid] = o;
-  }
+  walk_sm_fill(A, s_bt, s_boff, s_poff, s_poff2, s_xbit, tid, kCta);
+  const WalkSm sm{s_bt, s_boff, s_poff, s_poff2, s_xbit};
   __syncthreads();
   if (c >= A.C) return;  // whole teams only: no later CTA-wide barrier when TW < 8
   TeamState& S = s_team[team];
@@ -895,7 +920,7 @@ __global__ void __launch_bounds__(walk_cta_threads<TW>(), TW == 1 ? kWalkMinBloc
       d.old_eff = S.cb[v];
       d.old_cm = nodes_to_cand(S.cm[v], v);
       // few chains in flight (TW >= 8): more independent gathers per lane
-      const PairOut o = pair_argmax<TW >= 8 ? 4 : kEnumUnroll, WU>(A, v, S.pp[q], S.pc[q], S.prop, S.ppos, s_bt, s_boff, d);
+      const PairOut o = pair_argmax<TW >= 8 ? 4 : kEnumUnroll, WU>(A, v, S.pp[q], S.pc[q], S.prop, S.ppos, sm, d);
       walked += o.nw;
       enumerated += o.ne;
       if (lane == 0) {
@@ -1071,13 +1096,11 @@ __global__ void __launch_bounds__(1024, 1) walk_spec_kernel(WalkArgs A) {
   const int c = blockIdx.x;
   const int n = A.n;
   __shared__ FastDiv s_div[2];  // propose_swap's bounds n and n - 1
+  __shared__ uint32_t s_poff[kPoffMax], s_poff2[kPoffMax];
+  __shared__ uint64_t s_xbit[kMaxNodes * kXLevels];
   if (threadIdx.x < 2) s_div[threadIdx.x] = FastDiv::make((uint64_t)(n - threadIdx.x));
-  for (int i = tid; i < 65 * 9; i += kThreads) s_bt[i] = binom(i / 9, i % 9);
-  if (tid < 9) {
-    uint64_t o = 0;
-    for (int j = tid + 1; j <= A.s; ++j) o += binom(A.n - 1, j);
-    s_boff[tid] = o;
-  }
+  walk_sm_fill(A, s_bt, s_boff, s_poff, s_poff2, s_xbit, tid, kThreads);
+  const WalkSm sm{s_bt, s_boff, s_poff, s_poff2, s_xbit};
   if (tid == 0) {
     const Rng master{A.seeds[c]};
     Rng init = master.split(1);  // initial order: shuffle (sampler.cpp:83-86)
@@ -1226,7 +1249,7 @@ __global__ void __launch_bounds__(1024, 1) walk_spec_kernel(WalkArgs A) {
       dl.ynode = S.prop[lo];
       dl.old_eff = s_cb[v];
       dl.old_cm = nodes_to_cand(s_cm[v], v);
-      const PairOut o = pair_argmax<4, 8>(A, v, S.pp[qi], S.pc[qi], S.prop, S.ppos, s_bt, s_boff, dl);
+      const PairOut o = pair_argmax<4, 8>(A, v, S.pp[qi], S.pc[qi], S.prop, S.ppos, sm, dl);
       walked += o.nw;
       enumerated += o.ne;
       if (lane == 0) {
