@@ -178,20 +178,19 @@ struct bnmc_table {
   std::vector<double> h_w;
   // sorted rows for the walk path (K2W): eff desc + candidate masks, built
   // lazily after the priors are folded; PST of small predecessor counts.
-  DevBuf<double> seff;
-  DevBuf<uint64_t> scm;
+  // Sorted entries are 16-byte (eff bits, candidate mask) pairs: one 128-bit
+  // load per entry and lane in the walk.
+  DevBuf<ulonglong2> srow;  // [n][Sw]
   DevBuf<double> eff;  // eff = ls + PpfTable::sum in global-index order
   uint64_t Sw = 0;     // sorted row stride
-  DevBuf<double> yeff;  // delta-walk lists [n][n-1][Syw]
-  DevBuf<uint64_t> ycm;
+  DevBuf<ulonglong2> yrow;  // delta-walk lists [n][n-1][Syw]
   uint64_t Sy = 0, Syw = 0;
   bool ylists = false;
   // exclusion lists: row v's sorted entries without its strongest parent
   // (candidate bit xbit[v]); walked instead of the row when that parent is
   // not a predecessor [n][Sxw]
   // level j = 1..xlev excludes the row's j strongest parents (nested)
-  DevBuf<double> xeff;
-  DevBuf<uint64_t> xcm;
+  DevBuf<ulonglong2> xrow;
   DevBuf<uint64_t> xbit;  // [n][kXLevels] candidate bits of the strongest parents
   uint64_t Sx[kXLevels + 1] = {}, Sxw[kXLevels + 1] = {}, xoff[kXLevels + 1] = {};
   int xlev = 0;
@@ -476,7 +475,7 @@ TieCtx tie_ctx(const bnmc_table* t) {
 constexpr int kYThreads = 256, kYItems = 4;
 __global__ void __launch_bounds__(kYThreads) ylist_build_kernel(
     const double* __restrict__ seff, const uint64_t* __restrict__ scm, uint64_t S, uint64_t Sw,
-    int n, double* yeff, uint64_t* ycm, uint64_t Sy, uint64_t Syw, int* err,
+    int n, ulonglong2* yrow, uint64_t Sy, uint64_t Syw, int* err,
     const uint64_t* __restrict__ xbit = nullptr) {
   const int q = blockIdx.x, v = blockIdx.y;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -484,8 +483,7 @@ __global__ void __launch_bounds__(kYThreads) ylist_build_kernel(
   const double* re = seff + (uint64_t)v * Sw;
   const uint64_t* rc = scm + (uint64_t)v * Sw;
   const uint64_t lo = xbit ? (uint64_t)v * Syw : ((uint64_t)v * (n - 1) + q) * Syw;
-  double* oe = yeff + lo;
-  uint64_t* oc = ycm + lo;
+  ulonglong2* orow = yrow + lo;
   const uint64_t bit = xbit ? xbit[v] : 1ull << q;
   const uint64_t want = xbit ? 0ull : bit;  // keep entries whose (m & bit) == want
   uint64_t out = 0;
@@ -522,29 +520,27 @@ __global__ void __launch_bounds__(kYThreads) ylist_build_kernel(
 #pragma unroll
     for (int k = 0; k < kYItems; ++k)
       if (c0 + (uint64_t)tid * kYItems + k < S && (m[k] & bit) == want) {
-        if (pos < Sy) {
-          oe[pos] = e[k];
-          oc[pos] = m[k];
-        }
+        if (pos < Sy) orow[pos] = make_ulonglong2((unsigned long long)__double_as_longlong(e[k]), m[k]);
         ++pos;
       }
     out += s_warp[kYThreads / 32];
     __syncthreads();
   }
   if (tid == 0 && out != Sy) atomicExch(err, 6);
-  for (uint64_t i = Sy + tid; i < Syw; i += kYThreads) {
-    oe[i] = -INFINITY;
-    oc[i] = ~0ull;
-  }
+  for (uint64_t i = Sy + tid; i < Syw; i += kYThreads)
+    orow[i] = make_ulonglong2((unsigned long long)__double_as_longlong(-INFINITY), ~0ull);
 }
 
-// Padding of the sorted rows: eff -inf, mask ~0 (never admissible).
-__global__ void pad_sorted_kernel(double* seff, uint64_t* scm, uint64_t S, uint64_t Sw) {
+// Sorted rows, SoA (CUB output) -> AoS 16-byte entries, padded with
+// never-admissible entries (eff -inf, mask ~0) up to the row stride Sw.
+__global__ void pack_sorted_kernel(const double* __restrict__ seff, const uint64_t* __restrict__ scm,
+                                   ulonglong2* srow, uint64_t S, uint64_t Sw) {
   const uint64_t v = blockIdx.y;
-  for (uint64_t i = S + threadIdx.x; i < Sw; i += blockDim.x) {
-    seff[v * Sw + i] = -INFINITY;
-    scm[v * Sw + i] = ~0ull;
-  }
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < Sw;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    srow[v * Sw + i] = i < S ? make_ulonglong2((unsigned long long)__double_as_longlong(seff[v * S + i]),
+                                               scm[v * S + i])
+                             : make_ulonglong2((unsigned long long)__double_as_longlong(-INFINITY), ~0ull);
 }
 
 __global__ void eff64_kernel(const double* __restrict__ ls, const uint64_t* __restrict__ cmask,
@@ -630,8 +626,13 @@ void ensure_sorted(bnmc_table* t) {
   // bounds checks: row stride Sw >= S + one full round
   t->Sw = (t->S + 32 * kWalkPadRound + 31) / 32 * 32;
   const uint64_t NW = static_cast<uint64_t>(t->n) * t->Sw;
-  t->seff.alloc(NW);
-  t->scm.alloc(NW);
+  // CUB sorts into SoA temporaries (row stride S); the lists are built from
+  // them, then they are packed into the 16-byte entries the walk reads
+  DevBuf<double> seff;
+  DevBuf<uint64_t> scm;
+  seff.alloc(N);
+  scm.alloc(N);
+  t->srow.release();
   t->eff.alloc(N);  // eff in global-index order (kept: the enumeration gathers it)
   DevBuf<uint64_t> vals;
   vals.alloc(N);
@@ -643,17 +644,15 @@ void ensure_sorted(bnmc_table* t) {
   eff64_kernel<<<dim3(bx, t->n), 256, 0, t->stream>>>(t->ls.p, t->cmask.p, t->w.p, t->eff.p, vals.p,
                                                         t->n, t->S);
   CK(cudaGetLastError());
-  pad_sorted_kernel<<<dim3(1, t->n), 256, 0, t->stream>>>(t->seff.p, t->scm.p, t->S, t->Sw);
-  CK(cudaGetLastError());
   size_t temp_bytes = 0;
-  CK(cub::DeviceRadixSort::SortPairsDescending(nullptr, temp_bytes, t->eff.p, t->seff.p, vals.p,
-                                               t->scm.p, static_cast<int>(t->S), 0, 64, t->stream));
+  CK(cub::DeviceRadixSort::SortPairsDescending(nullptr, temp_bytes, t->eff.p, seff.p, vals.p,
+                                               scm.p, static_cast<int>(t->S), 0, 64, t->stream));
   DevBuf<uint8_t> temp;
   temp.alloc(std::max<size_t>(temp_bytes, 1));
   for (int v = 0; v < t->n; ++v) {
-    const uint64_t o = static_cast<uint64_t>(v) * t->S, ow = static_cast<uint64_t>(v) * t->Sw;
-    CK(cub::DeviceRadixSort::SortPairsDescending(temp.p, temp_bytes, t->eff.p + o, t->seff.p + ow,
-                                                 vals.p + o, t->scm.p + ow, static_cast<int>(t->S),
+    const uint64_t o = static_cast<uint64_t>(v) * t->S;
+    CK(cub::DeviceRadixSort::SortPairsDescending(temp.p, temp_bytes, t->eff.p + o, seff.p + o,
+                                                 vals.p + o, scm.p + o, static_cast<int>(t->S),
                                                  0, 64, t->stream));
   }
   // delta-walk lists, when they fit comfortably in device memory
@@ -666,15 +665,12 @@ void ensure_sorted(bnmc_table* t) {
   t->ylists = t->Sy > 0 && !(ydis && ydis[0] == '1') && t->ylist_mode != 0 &&
               (ybytes < free_b / 3 || t->ylist_mode == 1);
   if (t->ylists) {
-    t->yeff.alloc(static_cast<size_t>(ybytes / 16));
-    t->ycm.alloc(static_cast<size_t>(ybytes / 16));
+    t->yrow.alloc(static_cast<size_t>(ybytes / 16));
     ylist_build_kernel<<<dim3(t->n - 1, t->n), kYThreads, 0, t->stream>>>(
-        t->seff.p, t->scm.p, t->S, t->Sw, t->n, t->yeff.p, t->ycm.p, t->Sy, t->Syw,
-        t->rowcnt.p + 2 * t->n + 1);
+        seff.p, scm.p, t->S, t->S, t->n, t->yrow.p, t->Sy, t->Syw, t->rowcnt.p + 2 * t->n + 1);
     CK(cudaGetLastError());
   } else {
-    t->yeff.release();
-    t->ycm.release();
+    t->yrow.release();
   }
   // exclusion lists: the row's strongest parents = the candidates most
   // frequent among its top 256 sorted entries (a heuristic: results are exact
@@ -701,7 +697,7 @@ void ensure_sorted(bnmc_table* t) {
     std::vector<uint64_t> tops(static_cast<size_t>(t->n) * top);
     std::vector<uint64_t> bits(static_cast<size_t>(t->n) * kXLevels, 0);
     std::vector<uint64_t> masks(static_cast<size_t>(t->n) * t->xlev);
-    CK(cudaMemcpy2DAsync(tops.data(), top * 8, t->scm.p, t->Sw * 8, top * 8, t->n,
+    CK(cudaMemcpy2DAsync(tops.data(), top * 8, scm.p, t->S * 8, top * 8, t->n,
                          cudaMemcpyDeviceToHost, t->stream));
     CK(cudaStreamSynchronize(t->stream));
     for (int v = 0; v < t->n; ++v) {
@@ -720,8 +716,7 @@ void ensure_sorted(bnmc_table* t) {
       }
     }
     t->xbit.alloc(bits.size());
-    t->xeff.alloc(xtotal);
-    t->xcm.alloc(xtotal);
+    t->xrow.alloc(xtotal);
     DevBuf<uint64_t> d_masks;
     d_masks.alloc(masks.size());
     CK(cudaMemcpyAsync(t->xbit.p, bits.data(), 8 * bits.size(), cudaMemcpyHostToDevice, t->stream));
@@ -729,15 +724,21 @@ void ensure_sorted(bnmc_table* t) {
                        t->stream));
     for (int j = 1; j <= t->xlev; ++j) {
       ylist_build_kernel<<<dim3(1, t->n), kYThreads, 0, t->stream>>>(
-          t->seff.p, t->scm.p, t->S, t->Sw, t->n, t->xeff.p + t->xoff[j], t->xcm.p + t->xoff[j],
-          t->Sx[j], t->Sxw[j], t->rowcnt.p + 2 * t->n + 1, d_masks.p + (j - 1) * t->n);
+          seff.p, scm.p, t->S, t->S, t->n, t->xrow.p + t->xoff[j], t->Sx[j], t->Sxw[j],
+          t->rowcnt.p + 2 * t->n + 1, d_masks.p + (j - 1) * t->n);
       CK(cudaGetLastError());
     }
     CK(cudaStreamSynchronize(t->stream));  // host vectors and d_masks die here
   } else {
-    t->xeff.release();
-    t->xcm.release();
+    t->xrow.release();
     t->xbit.release();
+  }
+  // pack the sorted rows (the SoA temporaries are freed on return)
+  t->srow.alloc(NW);
+  {
+    const unsigned px = static_cast<unsigned>(std::min<uint64_t>((t->Sw + 255) / 256, 4096));
+    pack_sorted_kernel<<<dim3(px, t->n), 256, 0, t->stream>>>(seff.p, scm.p, t->srow.p, t->S, t->Sw);
+    CK(cudaGetLastError());
   }
   CK(cudaEventRecord(e1, t->stream));
   CK(cudaEventSynchronize(e1));
@@ -817,16 +818,13 @@ void launch_walk(bnmc_table* t, const WalkArgs& A, int C, int team_warps = 0,
 
 WalkArgs walk_args(bnmc_table* t) {
   WalkArgs A{};
-  A.seff = t->seff.p;
-  A.scm = t->scm.p;
+  A.srow = t->srow.p;
   A.eff = t->eff.p;
   A.Sw = t->Sw;
-  A.yeff = t->ylists ? t->yeff.p : nullptr;
-  A.ycm = t->ylists ? t->ycm.p : nullptr;
+  A.yrow = t->ylists ? t->yrow.p : nullptr;
   A.Sy = t->Sy;
   A.Syw = t->Syw;
-  A.xeff = t->xlev ? t->xeff.p : nullptr;
-  A.xcm = t->xlev ? t->xcm.p : nullptr;
+  A.xrow = t->xlev ? t->xrow.p : nullptr;
   A.xbit = t->xlev ? t->xbit.p : nullptr;
   A.xlev = t->xlev;
   for (int j = 0; j <= kXLevels; ++j) {

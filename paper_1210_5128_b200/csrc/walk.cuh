@@ -88,15 +88,14 @@ constexpr uint64_t kRecheckEvery = 100;  // sampler.cpp:105
     if (const int i = (base) + i##_h * (stride); i < (n))
 
 struct WalkArgs {
-  const double* __restrict__ seff;    // [n][Sw] eff, sorted descending per row, padded
-  const uint64_t* __restrict__ scm;   // [n][Sw] candidate masks in the same order
+  const ulonglong2* __restrict__ srow;  // [n][Sw] (eff bits, candidate mask), eff descending, padded
   const double* __restrict__ eff;     // [n][S] eff in global-index order
   uint64_t Sw;                        // sorted row stride (>= S + one walk round)
-  const double* __restrict__ yeff;    // [n][n-1][Syw] sorted entries of row v containing
-  const uint64_t* __restrict__ ycm;   //   candidate q (delta walks), or null
+  const ulonglong2* __restrict__ yrow;  // [n][n-1][Syw] sorted entries of row v containing
+                                       //   candidate q (delta walks), or null
   uint64_t Sy, Syw;                   // entries per list, padded stride
-  const double* __restrict__ xeff;    // exclusion lists, level j at xoff[j]: [n][Sxw[j]]
-  const uint64_t* __restrict__ xcm;   //   row v without its j strongest parents, or null
+  const ulonglong2* __restrict__ xrow;  // exclusion lists, level j at xoff[j]: [n][Sxw[j]]
+                                       //   row v without its j strongest parents, or null
   const uint64_t* __restrict__ xbit;  // [n][kXLevels] candidate bits of those parents
   int xlev;                           // levels built (0..kXLevels)
   uint64_t xoff[kXLevels + 1];
@@ -233,7 +232,7 @@ struct WalkHit {
 // One walk round of U entries per lane at sorted indices [base, base + 32U);
 // advances base; true once the first admissible entry is found.
 template <int U, bool kFloor = false>
-__device__ BNMC_WALK_ROUND_INLINE bool walk_round(const double* re, const uint64_t* rc, uint64_t ncp,
+__device__ BNMC_WALK_ROUND_INLINE bool walk_round(const ulonglong2* rr, uint64_t ncp,
                                            uint32_t S, uint32_t& base, int lane, WalkHit& h,
                                            double floor = -INFINITY, bool* exhausted = nullptr) {
   if (base >= S) return false;
@@ -242,8 +241,9 @@ __device__ BNMC_WALK_ROUND_INLINE bool walk_round(const double* re, const uint64
 #pragma unroll
   for (int u = 0; u < U; ++u) {
     const uint32_t i = base + u * 32 + lane;  // < Sw < 2^32: rows are padded by one round
-    e[u] = __ldg(re + i);
-    c[u] = __ldg(rc + i);
+    const ulonglong2 x = __ldg(rr + i);  // one 16-byte (eff, mask) entry
+    e[u] = __longlong_as_double((long long)x.x);
+    c[u] = x.y;
   }
   // first group holding an admissible entry (at or above `floor`); its values
   // selected without dynamic register indexing, then one set of shuffles
@@ -287,7 +287,7 @@ __device__ BNMC_WALK_ROUND_INLINE bool walk_round(const double* re, const uint64
 // Admissible entries after sorted index `start` holding exactly kstar: the
 // reference keeps the first of them in predecessor-position order. Returns the
 // chosen candidate mask; *ties = number of further admissible equal entries.
-__device__ __noinline__ uint64_t collect_ties(const double* re, const uint64_t* rc, uint64_t ncp,
+__device__ __noinline__ uint64_t collect_ties(const ulonglong2* rr, uint64_t ncp,
                                               uint64_t S, uint64_t start, double kstar,
                                               uint64_t kcm, int v, const uint8_t* ppos, int* ties_out) {
   const int lane = threadIdx.x & 31;
@@ -295,8 +295,9 @@ __device__ __noinline__ uint64_t collect_ties(const double* re, const uint64_t* 
   int ties = 0;
   for (uint64_t i0 = start + 1;; i0 += 32) {
     const uint64_t i = i0 + lane;
-    const bool eq = i < S && __ldg(re + i) == kstar;
-    const uint64_t cm = eq ? __ldg(rc + i) : ~0ull;
+    const ulonglong2 x = i < S ? __ldg(rr + i) : make_ulonglong2(0ull, ~0ull);
+    const bool eq = i < S && __longlong_as_double((long long)x.x) == kstar;
+    const uint64_t cm = eq ? x.y : ~0ull;
     const bool adm = eq && (cm & ncp) == 0;
     const unsigned bal = __ballot_sync(0xffffffffu, adm);
     if (bal) {
@@ -410,7 +411,7 @@ __device__ __forceinline__ void walk_sm_fill(const WalkArgs& A, uint64_t* bt, ui
   }
   for (int i = tid; i < A.pc + 2; i += nthreads) poff[i] = A.pst_off[i];
   for (int i = tid; i < A.pe + 1; i += nthreads) poff2[i] = A.pst2_off[i];
-  if (A.xeff)
+  if (A.xrow)
     for (int i = tid; i < A.n * kXLevels; i += nthreads) xbit[i] = A.xbit[i];
 }
 
@@ -437,14 +438,13 @@ __device__ PairOut pair_argmax(const WalkArgs& A, int v, int p, uint64_t cpred, 
   uint32_t walked_n = 0;
   if (p > A.pe) {
     const uint64_t ncp = ~cpred;
-    if (d.on && A.yeff) {
+    if (d.on && A.yrow) {
       // ---- delta walk: only sets containing Y can beat the current best, so
       // walk row v's list of entries containing Y down to the current best's
       // value (SURVEY §7 "incremental middle rows")
       const int qy = d.ynode - (d.ynode > v);
       const uint64_t lo = (uint64_t)(uint32_t)(v * (A.n - 1) + qy) * A.Syw32;
-      const double* ye = A.yeff + lo;
-      const uint64_t* yc = A.ycm + lo;
+      const ulonglong2* yr = A.yrow + lo;
       r.eff = d.old_eff;
       r.cm = d.old_cm;
       r.tied = 0;
@@ -455,15 +455,15 @@ __device__ PairOut pair_argmax(const WalkArgs& A, int v, int p, uint64_t cpred, 
       bool done = false;
       uint32_t base = 0;
       const uint32_t Sy = (uint32_t)A.Sy;
-      if (!walk_round<1, true>(ye, yc, ncp, Sy, base, lane, h, d.old_eff, &done) && !done &&
-          !walk_round<2, true>(ye, yc, ncp, Sy, base, lane, h, d.old_eff, &done) && !done)
-        while (base < Sy && !done && !walk_round<WU, true>(ye, yc, ncp, Sy, base, lane, h, d.old_eff, &done)) {
+      if (!walk_round<1, true>(yr, ncp, Sy, base, lane, h, d.old_eff, &done) && !done &&
+          !walk_round<2, true>(yr, ncp, Sy, base, lane, h, d.old_eff, &done) && !done)
+        while (base < Sy && !done && !walk_round<WU, true>(yr, ncp, Sy, base, lane, h, d.old_eff, &done)) {
         }
       r.nw = base;
       if (h.start == ~0ull) return r;  // no set containing Y reaches the current best
       int ties = 0;
       uint64_t cm = h.kcm;
-      if (!h.next_differs) cm = collect_ties(ye, yc, ncp, A.Sy, h.start, h.kstar, h.kcm, v, ppos, &ties);
+      if (!h.next_differs) cm = collect_ties(yr, ncp, A.Sy, h.start, h.kstar, h.kcm, v, ppos, &ties);
       if (h.kstar > d.old_eff) {
         r.eff = h.kstar;
         r.cm = cm;
@@ -479,20 +479,17 @@ __device__ PairOut pair_argmax(const WalkArgs& A, int v, int p, uint64_t cpred, 
     // predecessor, no admissible set contains it: walk the row's exclusion
     // list (same admissible entries in the same order, the others skipped).
     int xj = 0;  // leading strongest parents missing from the predecessors
-    if (A.xeff)
+    if (A.xrow)
       while (xj < A.xlev && (ncp & sm.xbit[v * kXLevels + xj])) ++xj;
-    const double* re;
-    const uint64_t* rc;
+    const ulonglong2* rr;
     uint32_t S;
     if (xj) {
       const uint64_t ro = A.xoff[xj] + (uint64_t)(uint32_t)v * A.Sxw32[xj];
-      re = A.xeff + ro;
-      rc = A.xcm + ro;
+      rr = A.xrow + ro;
       S = A.Sx32[xj];
     } else {
       const uint64_t ro = (uint64_t)(uint32_t)v * A.Sw32;
-      re = A.seff + ro;
-      rc = A.scm + ro;
+      rr = A.srow + ro;
       S = A.S32;
     }
     const uint32_t lim =
@@ -501,10 +498,10 @@ __device__ PairOut pair_argmax(const WalkArgs& A, int v, int p, uint64_t cpred, 
     // Rounds grow 32, 64, 128, then 32 * WU entries: most first admissible
     // entries sit in the first 32, deep walks still get WU loads per lane in flight.
     uint32_t base = 0;
-    if (walk_round<1>(re, rc, ncp, S, base, lane, h) || walk_round<2>(re, rc, ncp, S, base, lane, h) ||
-        walk_round<4>(re, rc, ncp, S, base, lane, h)) {
+    if (walk_round<1>(rr, ncp, S, base, lane, h) || walk_round<2>(rr, ncp, S, base, lane, h) ||
+        walk_round<4>(rr, ncp, S, base, lane, h)) {
     } else {
-      while (base < lim && base < S && !walk_round<WU>(re, rc, ncp, S, base, lane, h)) {
+      while (base < lim && base < S && !walk_round<WU>(rr, ncp, S, base, lane, h)) {
       }
     }
     walked_n = base;
@@ -518,7 +515,7 @@ __device__ PairOut pair_argmax(const WalkArgs& A, int v, int p, uint64_t cpred, 
       if (h.next_differs) return r;
       // Tie collection (rare): admissible entries after `start` with eff == kstar.
       int ties = 0;
-      r.cm = collect_ties(re, rc, ncp, S, h.start, h.kstar, h.kcm, v, ppos, &ties);
+      r.cm = collect_ties(rr, ncp, S, h.start, h.kstar, h.kcm, v, ppos, &ties);
       r.tied = ties > 0;
       return r;
     }
@@ -872,10 +869,10 @@ __global__ void __launch_bounds__(walk_cta_threads<TW>(), TW == 1 ? kWalkMinBloc
         // best set containing Y) is below its current best keeps its best: it
         // is dropped here, one load per row in parallel, instead of costing a
         // pair (pair_argmax's delta early exit, same test)
-        dl[h] = take[h] && !BNMC_FRESH && p > lo && p < hi && (p <= A.pe || A.yeff) &&
+        dl[h] = take[h] && !BNMC_FRESH && p > lo && p < hi && (p <= A.pe || A.yrow) &&
                 !(S.tied & bit[h]) && !((S.cm[v] >> xnode) & 1ull);
         if (dl[h] && p > A.pe &&
-            __ldg(A.yeff + (uint64_t)(uint32_t)(v * (n - 1) + ynode - (ynode > v)) * A.Syw32) <
+            __longlong_as_double((long long)__ldg(&A.yrow[(uint64_t)(uint32_t)(v * (n - 1) + ynode - (ynode > v)) * A.Syw32].x)) <
                 S.cb[v])
           take[h] = false;
       }
@@ -1188,10 +1185,10 @@ __global__ void __launch_bounds__(1024, 1) walk_spec_kernel(WalkArgs A) {
         take[h] = p < n && ((p >= lo && p <= hi) || (p > hi && (s_tied & bit[h])));
         // delta rows whose Y-list head is below the current best keep it
         // (as in walk_chain_kernel's pair list)
-        dl[h] = take[h] && t > 0 && p > lo && p < hi && (p <= A.pe || A.yeff) &&
+        dl[h] = take[h] && t > 0 && p > lo && p < hi && (p <= A.pe || A.yrow) &&
                 !(s_tied & bit[h]) && !((s_cm[v] >> xnode) & 1ull);
         if (dl[h] && p > A.pe &&
-            __ldg(A.yeff + (uint64_t)(uint32_t)(v * (n - 1) + ynode - (ynode > v)) * A.Syw32) <
+            __longlong_as_double((long long)__ldg(&A.yrow[(uint64_t)(uint32_t)(v * (n - 1) + ynode - (ynode > v)) * A.Syw32].x)) <
                 s_cb[v])
           take[h] = false;
       }
