@@ -734,6 +734,8 @@ struct TeamState {
   double tmin;  // tracker minimum when full (-inf before), kept by the insert path
   double tbest;                    // tracker maximum (slot tracker: trace rows)
   uint8_t tord[32];                // slot tracker: slot of the e-th best entry
+  uint8_t qa[32], qb[32];          // proposals of the current batch of 32 iterations
+  double qu[32];                   // their accept draws next_unit_open()
   unsigned long long acc;
   int np, a, b, accept, tcount, amb;
 };
@@ -765,6 +767,47 @@ __device__ __noinline__ void init_team_state(TeamState& S, const WalkArgs& A, in
   S.tbest = -INFINITY;
   S.acc = 0;
   S.cur_total = 0.0;
+}
+
+constexpr int kPropBatch = 32;  // iterations whose proposals are drawn together
+
+// The next kPropBatch iterations' propose_swap draws (split(2) stream: a =
+// next_below(n), b = next_below(n - 1), b += b >= a) and mh_accept draws
+// (split(3) stream: next_unit_open), lane i for iteration i of the batch, by
+// direct indexing of the splitmix64 sequence (rng.hpp:14-45). Exact: when any
+// draw of the batch falls below next_below's rejection threshold, lane 0
+// redraws the batch sequentially with rejection.
+__device__ __noinline__ void draw_proposal_batch(TeamState& S, const FastDiv* div, int lane) {
+  constexpr uint64_t kGamma = 0x9E3779B97F4A7C15ull;
+  const uint64_t s0 = S.rng, sa = S.arng;
+  const uint64_t x0 = Rng::mix(s0 + kGamma * (uint64_t)(2 * lane + 1));
+  const uint64_t x1 = Rng::mix(s0 + kGamma * (uint64_t)(2 * lane + 2));
+  const uint64_t xu = Rng::mix(sa + kGamma * (uint64_t)(lane + 1));
+  S.qu[lane] = ((double)(xu >> 11) + 0.5) * 0x1.0p-53;
+  if (__all_sync(0xffffffffu, x0 >= div[0].thr && x1 >= div[1].thr)) {
+    const int a = (int)div[0].mod(x0);
+    int b = (int)div[1].mod(x1);
+    if (b >= a) ++b;
+    S.qa[lane] = (uint8_t)a;
+    S.qb[lane] = (uint8_t)b;
+    __syncwarp();
+    if (lane == 0) S.rng = s0 + kGamma * (uint64_t)(2 * kPropBatch);
+  } else {
+    __syncwarp();
+    if (lane == 0) {
+      Rng pr{s0};
+      for (int i = 0; i < kPropBatch; ++i) {
+        const int a = (int)pr.next_below(div[0]);
+        int b = (int)pr.next_below(div[1]);
+        if (b >= a) ++b;
+        S.qa[i] = (uint8_t)a;
+        S.qb[i] = (uint8_t)b;
+      }
+      S.rng = pr.s;
+    }
+  }
+  if (lane == 0) S.arng = sa + kGamma * (uint64_t)kPropBatch;
+  __syncwarp();
 }
 
 template <int TW>
@@ -818,24 +861,25 @@ __global__ void __launch_bounds__(walk_cta_threads<TW>(), TW == 1 ? kWalkMinBloc
     // fresh: score every row of S.order, no proposal (recomputed at each use:
     // a live predicate costs the production kernel a register)
 #define BNMC_FRESH (t == 0 || (RC && rc))
-    // ---- proposal: propose_swap (sampler.cpp:43-52) from the split(2) stream
+    // ---- proposal: propose_swap (sampler.cpp:43-52) from the split(2) stream.
+    // The proposal and accept streams do not depend on the chain's state, and
+    // splitmix64's k-th draw is mix(state + k*gamma): every 32 iterations the
+    // team's first warp draws the next 32 proposals and accept draws at once,
+    // one iteration per lane. next_below's rejection (probability ~n/2^64) is
+    // detected exactly; such a batch is redrawn in sequence by lane 0.
+    if (!BNMC_FRESH && twarp == 0 && ((t - 1) & (kPropBatch - 1)) == 0)
+      draw_proposal_batch(S, s_div, lane);
     if (ttid == 0) {
       int a = 0, b = n - 1;
       if (!BNMC_FRESH) {
-        Rng pr{S.rng};
-        a = (int)pr.next_below(s_div[0]);
-        b = (int)pr.next_below(s_div[1]);
-        if (b >= a) ++b;
-        S.rng = pr.s;
+        const int k = (int)((t - 1) & (kPropBatch - 1));
+        a = S.qa[k];
+        b = S.qb[k];
         if (A.thr) {
           // issued now, consumed after the scan: the load overlaps the pair work
           thr_t = A.thr[(uint64_t)c * (A.iters + 1) + t];
         } else {
-          // mh_accept's draw (sampler.cpp:54-56): one per iteration, split(3);
-          // its logarithm only when the decision needs it (mh_accept_dev)
-          Rng ar{S.arng};
-          thr_t = ar.next_unit_open();
-          S.arng = ar.s;
+          thr_t = S.qu[k];  // mh_accept's draw; its logarithm only when needed (mh_accept_dev)
         }
       }
       S.a = a;
