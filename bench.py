@@ -365,17 +365,24 @@ def run_ours(args):
         comm = D.Comm(rank, world, local)
     data, pri, cfg, truth = P.baseline_instance(args.config)
     cfg.device = local
-    # ---- precompute: K1 split over the ranks + NCCL all-reduce, then the per-row sort
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    cache = D.build_table_comm(data, cfg, pri, comm) if dist_on else P.ScoreCache.build(data, cfg, pri)
-    cfg.iterations, cfg.scan_mode = 1, 2
-    # binds priors, builds the sorted rows (pageable 1-chain result buffer: no
-    # page-locked allocation inside the precompute timing)
-    P.run_chains_batch(cache, pri, [1], cfg,
-                       P.api.ChainBatch.allocate(1, 1, data.n, cfg.track_top, pinned=False))
-    torch.cuda.synchronize()
-    pre_s = time.perf_counter() - t0
+    # ---- precompute: K1 split over the ranks + NCCL all-reduce, then the per-row
+    # sort and walk lists. Built twice: the first build in a fresh process also
+    # pays the driver's first multi-GB allocations (precompute_cold_s); the
+    # second is the steady-state figure (precompute_s).
+    def precompute():
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        c_ = D.build_table_comm(data, cfg, pri, comm) if dist_on else P.ScoreCache.build(data, cfg, pri)
+        cfg.iterations, cfg.scan_mode = 1, 2
+        # binds priors, builds the sorted rows (pageable 1-chain result buffer: no
+        # page-locked allocation inside the precompute timing)
+        P.run_chains_batch(c_, pri, [1], cfg,
+                           P.api.ChainBatch.allocate(1, 1, data.n, cfg.track_top, pinned=False))
+        torch.cuda.synchronize()
+        return c_, time.perf_counter() - t0
+    cache, pre_cold_s = precompute()
+    cache.close()
+    cache, pre_s = precompute()
     k1, fold = C.c_float(), C.c_float()
     _lib.check(_lib.lib().bnmc_gpu_table_build_ms(cache.handle, C.byref(k1), C.byref(fold)))
     Cn, I = args.chains, args.iters
@@ -494,7 +501,8 @@ def run_ours(args):
                      "walked_per_pair": walked / max(1, pairs),
                      "enumerated_per_pair": enumerated / max(1, pairs),
                      "chains_replayed_exact": replayed},
-            "precompute_s": pre_s, "precompute_kernel_ms": k1_ms, "fold_ms": fold.value,
+            "precompute_s": pre_s, "precompute_cold_s": pre_cold_s, "precompute_kernel_ms": k1_ms,
+            "fold_ms": fold.value,
             "gpu_launches": int(launches),
             "best_total": best["best_total"], "best_chain_seed": best["seed"],
             "cpu_baseline": cpu,
