@@ -55,6 +55,10 @@ constexpr int kWalkMinBlocks1 = BNMC_WALK_MINB1;  // CTAs per SM targeted for on
 #ifndef BNMC_ENUM_UNROLL
 #define BNMC_ENUM_UNROLL 1
 #endif
+#ifndef BNMC_R1
+#define BNMC_R1 1
+#endif
+constexpr int kR1 = BNMC_R1;  // entries per lane of a walk's first round (then 2x, then 4/WU)
 constexpr int kEnumUnroll = BNMC_ENUM_UNROLL;  // independent gathers per lane per enumeration step
 constexpr uint64_t kEnumMax = 64;          // enumerate when S(p,s) <= this (walk above)
 // Rows with kEnumMax < S(p,s) <= walk cap walk at most kWalkBudget * S(p,s)
@@ -397,12 +401,27 @@ struct WalkSm {
   const uint32_t* poff;   // pst_off [pc + 2]
   const uint32_t* poff2;  // pst2_off [pe + 1]
   const uint64_t* xbit;   // [n][kXLevels]
+  const uint32_t* cap;    // [kMaxNodes] walk cap by predecessor count (capped walks)
+  const uint64_t* lm;     // [kMaxNodes] (1 << v) - 1: candidate <-> node mask remaps
 };
+
+// nodes_to_cand / cand_to_nodes (common.cuh) with row v's low mask from a table.
+__device__ __forceinline__ uint64_t n2c(uint64_t pm, uint64_t lm) { return (pm & lm) | ((pm >> 1) & ~lm); }
+__device__ __forceinline__ uint64_t c2n(uint64_t cm, uint64_t lm) {
+  return (cm & lm) | ((cm << 1) & ~((lm << 1) | 1ull));
+}
 constexpr int kPoffMax = kMaxNodes + 2;
 
 // Fill the WalkSm tables (every thread of the CTA; a barrier must follow).
 __device__ __forceinline__ void walk_sm_fill(const WalkArgs& A, uint64_t* bt, uint64_t* boff, uint32_t* poff,
-                                             uint32_t* poff2, uint64_t* xbit, int tid, int nthreads) {
+                                             uint32_t* poff2, uint64_t* xbit, uint32_t* cap, uint64_t* lm,
+                                             int tid, int nthreads) {
+  for (int p = tid; p < kMaxNodes; p += nthreads) {
+    cap[p] = p <= A.pc ? (uint32_t)min((uint64_t)0xFFFFFFFFu,
+                                       (uint64_t)A.wbud * (A.pst_off[p + 1] - A.pst_off[p]))
+                       : 0xFFFFFFFFu;
+    lm[p] = (1ull << p) - 1ull;
+  }
   for (int i = tid; i < 65 * 9; i += nthreads) bt[i] = binom(i / 9, i % 9);
   if (tid < 9) {
     uint64_t o = 0;
@@ -455,8 +474,8 @@ __device__ PairOut pair_argmax(const WalkArgs& A, int v, int p, uint64_t cpred, 
       bool done = false;
       uint32_t base = 0;
       const uint32_t Sy = (uint32_t)A.Sy;
-      if (!walk_round<1, true>(yr, ncp, Sy, base, lane, h, d.old_eff, &done) && !done &&
-          !walk_round<2, true>(yr, ncp, Sy, base, lane, h, d.old_eff, &done) && !done)
+      if (!walk_round<kR1, true>(yr, ncp, Sy, base, lane, h, d.old_eff, &done) && !done &&
+          !walk_round<2 * kR1, true>(yr, ncp, Sy, base, lane, h, d.old_eff, &done) && !done)
         while (base < Sy && !done && !walk_round<WU, true>(yr, ncp, Sy, base, lane, h, d.old_eff, &done)) {
         }
       r.nw = base;
@@ -492,13 +511,12 @@ __device__ PairOut pair_argmax(const WalkArgs& A, int v, int p, uint64_t cpred, 
       rr = A.srow + ro;
       S = A.S32;
     }
-    const uint32_t lim =
-        p <= A.pc ? (uint32_t)min((uint64_t)S, (uint64_t)A.wbud * (sm.poff[p + 1] - sm.poff[p])) : S;
+    const uint32_t lim = min(S, sm.cap[p]);
     WalkHit h;
     // Rounds grow 32, 64, 128, then 32 * WU entries: most first admissible
     // entries sit in the first 32, deep walks still get WU loads per lane in flight.
     uint32_t base = 0;
-    if (walk_round<1>(rr, ncp, S, base, lane, h) || walk_round<2>(rr, ncp, S, base, lane, h) ||
+    if (walk_round<kR1>(rr, ncp, S, base, lane, h) || walk_round<2 * kR1>(rr, ncp, S, base, lane, h) ||
         walk_round<4>(rr, ncp, S, base, lane, h)) {
     } else {
       while (base < lim && base < S && !walk_round<WU>(rr, ncp, S, base, lane, h)) {
@@ -835,20 +853,22 @@ __global__ void __launch_bounds__(walk_cta_threads<TW>(), TW == 1 ? kWalkMinBloc
   __shared__ FastDiv s_div[2];  // propose_swap's bounds n and n - 1
   __shared__ uint32_t s_poff[kPoffMax], s_poff2[kPoffMax];
   __shared__ uint64_t s_xbit[kMaxNodes * kXLevels];
+  __shared__ uint32_t s_cap[kMaxNodes];
+  __shared__ uint64_t s_lm[kMaxNodes];
   const int tid = threadIdx.x, lane = tid & 31;
   const int team = (tid >> 5) / TW, twarp = (tid >> 5) % TW, ttid = tid - team * TW * 32;
   const int c = blockIdx.x * kTeams + team;
   const int n = A.n;
   if (tid < 2) s_div[tid] = FastDiv::make((uint64_t)(n - tid));
-  walk_sm_fill(A, s_bt, s_boff, s_poff, s_poff2, s_xbit, tid, kCta);
-  const WalkSm sm{s_bt, s_boff, s_poff, s_poff2, s_xbit};
+  walk_sm_fill(A, s_bt, s_boff, s_poff, s_poff2, s_xbit, s_cap, s_lm, tid, kCta);
+  const WalkSm sm{s_bt, s_boff, s_poff, s_poff2, s_xbit, s_cap, s_lm};
   __syncthreads();
   if (c >= A.C) return;  // whole teams only: no later CTA-wide barrier when TW < 8
   TeamState& S = s_team[team];
   const bool score_only = A.perms != nullptr;
   if (ttid == 0) init_team_state(S, A, c, n, score_only);
   team_sync<TW>(team);
-  unsigned long long walked = 0, enumerated = 0;  // statistics (lane 0 of each warp)
+  uint32_t walked = 0, enumerated = 0;  // statistics per warp (u32: statistics only)
   unsigned long long pairs = 0;
   double thr_t = 0.0;
   const uint64_t T = score_only ? 0 : A.iters;
@@ -959,13 +979,13 @@ __global__ void __launch_bounds__(walk_cta_threads<TW>(), TW == 1 ? kWalkMinBloc
       d.ypos = lo;
       d.ynode = S.prop[lo];
       d.old_eff = S.cb[v];
-      d.old_cm = nodes_to_cand(S.cm[v], v);
+      d.old_cm = n2c(S.cm[v], sm.lm[v]);
       // few chains in flight (TW >= 8): more independent gathers per lane
       const PairOut o = pair_argmax<TW >= 8 ? 4 : kEnumUnroll, WU>(A, v, S.pp[q], S.pc[q], S.prop, S.ppos, sm, d);
       walked += o.nw;
       enumerated += o.ne;
       if (lane == 0) {
-        S.pm[v] = cand_to_nodes(o.cm, v);
+        S.pm[v] = c2n(o.cm, sm.lm[v]);
         S.pb[v] = o.eff;
         S.pt[q] = (uint8_t)o.tied;
       }
@@ -1083,8 +1103,8 @@ __global__ void __launch_bounds__(walk_cta_threads<TW>(), TW == 1 ? kWalkMinBloc
     }
   }
   if (lane == 0 && A.stat) {
-    atomicAdd(A.stat + 1, walked);
-    atomicAdd(A.stat + 2, enumerated);
+    atomicAdd(A.stat + 1, (unsigned long long)walked);
+    atomicAdd(A.stat + 2, (unsigned long long)enumerated);
     if (twarp == 0) atomicAdd(A.stat, pairs);
   }
 }
@@ -1139,9 +1159,11 @@ __global__ void __launch_bounds__(1024, 1) walk_spec_kernel(WalkArgs A) {
   __shared__ FastDiv s_div[2];  // propose_swap's bounds n and n - 1
   __shared__ uint32_t s_poff[kPoffMax], s_poff2[kPoffMax];
   __shared__ uint64_t s_xbit[kMaxNodes * kXLevels];
+  __shared__ uint32_t s_cap[kMaxNodes];
+  __shared__ uint64_t s_lm[kMaxNodes];
   if (threadIdx.x < 2) s_div[threadIdx.x] = FastDiv::make((uint64_t)(n - threadIdx.x));
-  walk_sm_fill(A, s_bt, s_boff, s_poff, s_poff2, s_xbit, tid, kThreads);
-  const WalkSm sm{s_bt, s_boff, s_poff, s_poff2, s_xbit};
+  walk_sm_fill(A, s_bt, s_boff, s_poff, s_poff2, s_xbit, s_cap, s_lm, tid, kThreads);
+  const WalkSm sm{s_bt, s_boff, s_poff, s_poff2, s_xbit, s_cap, s_lm};
   if (tid == 0) {
     const Rng master{A.seeds[c]};
     Rng init = master.split(1);  // initial order: shuffle (sampler.cpp:83-86)
@@ -1289,12 +1311,12 @@ __global__ void __launch_bounds__(1024, 1) walk_spec_kernel(WalkArgs A) {
       dl.ypos = lo;
       dl.ynode = S.prop[lo];
       dl.old_eff = s_cb[v];
-      dl.old_cm = nodes_to_cand(s_cm[v], v);
+      dl.old_cm = n2c(s_cm[v], sm.lm[v]);
       const PairOut o = pair_argmax<4, 8>(A, v, S.pp[qi], S.pc[qi], S.prop, S.ppos, sm, dl);
       walked += o.nw;
       enumerated += o.ne;
       if (lane == 0) {
-        S.pm[v] = cand_to_nodes(o.cm, v);
+        S.pm[v] = c2n(o.cm, sm.lm[v]);
         S.pb[v] = o.eff;
         S.pt[qi] = (uint8_t)o.tied;
       }
