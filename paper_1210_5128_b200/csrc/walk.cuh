@@ -869,8 +869,7 @@ __global__ void __launch_bounds__(walk_cta_threads<TW>(), TW == 1 ? kWalkMinBloc
   if (ttid == 0) init_team_state(S, A, c, n, score_only);
   team_sync<TW>(team);
   uint32_t walked = 0, enumerated = 0;  // statistics per warp (u32: statistics only)
-  unsigned long long pairs = 0;
-  double thr_t = 0.0;
+  uint32_t pairs = 0;
   const uint64_t T = score_only ? 0 : A.iters;
   // rc: a debug_recheck pass (sampler.cpp:105-110) after iteration t-1: the
   // current order is re-scored from scratch (every row, full walks, no delta
@@ -895,12 +894,6 @@ __global__ void __launch_bounds__(walk_cta_threads<TW>(), TW == 1 ? kWalkMinBloc
         const int k = (int)((t - 1) & (kPropBatch - 1));
         a = S.qa[k];
         b = S.qb[k];
-        if (A.thr) {
-          // issued now, consumed after the scan: the load overlaps the pair work
-          thr_t = A.thr[(uint64_t)c * (A.iters + 1) + t];
-        } else {
-          thr_t = S.qu[k];  // mh_accept's draw; its logarithm only when needed (mh_accept_dev)
-        }
       }
       S.a = a;
       S.b = b;
@@ -1022,11 +1015,13 @@ __global__ void __launch_bounds__(walk_cta_threads<TW>(), TW == 1 ? kWalkMinBloc
         atomicCAS(A.stat + 3, 0ull, (unsigned long long)(t - 1));
         atomicExch(A.error, kErrDrift);
       }
-      // mh_accept, sampler.cpp:54-56: log10(u) < new - old (thr_t = host glibc
-      // log10(u) when A.thr, else u itself)
+      // mh_accept, sampler.cpp:54-56: log10(u) < new - old, with the host's glibc
+      // log10(u) when A.thr, else the batch's draw u (logarithm only when needed)
       const double delta = tot - S.cur_total;
       bool acc = true;
-      if (!BNMC_FRESH) acc = A.thr ? thr_t < delta : mh_accept_dev(thr_t, delta, A.accept_tol, &S.amb);
+      if (!BNMC_FRESH)
+        acc = A.thr ? A.thr[(uint64_t)c * (A.iters + 1) + t] < delta
+                    : mh_accept_dev(S.qu[(t - 1) & (kPropBatch - 1)], delta, A.accept_tol, &S.amb);
       S.accept = acc;
     }
     team_sync<TW>(team);
@@ -1105,7 +1100,7 @@ __global__ void __launch_bounds__(walk_cta_threads<TW>(), TW == 1 ? kWalkMinBloc
   if (lane == 0 && A.stat) {
     atomicAdd(A.stat + 1, (unsigned long long)walked);
     atomicAdd(A.stat + 2, (unsigned long long)enumerated);
-    if (twarp == 0) atomicAdd(A.stat, pairs);
+    if (twarp == 0) atomicAdd(A.stat, (unsigned long long)pairs);
   }
 }
 
