@@ -963,9 +963,9 @@ __global__ void __launch_bounds__(walk_cta_threads<TW>(), TW == 1 ? kWalkMinBloc
       if (lane == 31) S.np = cnt;
     }
     team_sync<TW>(team);
-    const int np = S.np;
-    // ---- exact argmax of every rescanned row, one warp per pair
-    for (int q = twarp; q < np; q += TW) {
+    // ---- exact argmax of every rescanned row, one warp per pair (the bound is
+    // re-read from shared memory: a register for it was spilled around pairs)
+    for (int q = twarp; q < *reinterpret_cast<volatile int*>(&S.np); q += TW) {
       const int v = S.pv[q];
       DeltaIn d;
       d.on = S.pd[q] != 0;
@@ -983,12 +983,13 @@ __global__ void __launch_bounds__(walk_cta_threads<TW>(), TW == 1 ? kWalkMinBloc
         S.pt[q] = (uint8_t)o.tied;
       }
     }
-    pairs += np;
+    pairs += S.np;
     team_sync<TW>(team);
     // ---- total in ascending node order (engine.cpp:95-96), tie bits, mh_accept
     if (twarp == 0) {
       // tie bits of the rescanned rows (distinct nodes: order-free), by the warp
       uint64_t clr = 0, set = 0;
+      const int np = S.np;
       BNMC_FOR_NODES(q, lane, 32, np) {
         const uint64_t b = 1ull << S.pv[q];
         clr |= b;

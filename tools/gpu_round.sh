@@ -14,7 +14,7 @@ ref) timeout 900 python bench.py --impl reference > $D/bench_ref.json 2> $D/benc
 dist) timeout 600 python bench.py --force-dist --steps 2 --warmup 1 --no-extras --no-cpu-baseline --parity-chains 0 > $D/bench_dist.json 2> $D/bench_dist.err ;;
 launches) timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $D/launches.csv \
     python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-extras --parity-chains 0 > $D/bench_ncu.log 2>&1 ;;
-ncu) timeout 1200 ncu --set full --clock-control none --import-source on -k regex:walk_chain -s 1 -c 1 \
+ncu) timeout 1200 ncu --set full --clock-control none --import-source on -k regex:walk_chain -s 2 -c 1 \
     -o $D/walk_bench -f python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-extras --parity-chains 0 > $D/ncu_walk.log 2>&1 ;;
 ncuk1) timeout 900 ncu --set full --clock-control none --import-source on -k regex:k1_kernel -c 1 \
     -o $D/k1 -f python tools/profile_run.py 1 2 > $D/ncu_k1.log 2>&1 ;;
