@@ -18,8 +18,11 @@ t0 = time.perf_counter()
 cache = P.ScoreCache.build(data, cfg, pri)
 print(f"build {time.perf_counter() - t0:.3f}s", flush=True)
 cfg.iterations = iters
-if os.environ.get("BNMC_DEEP"):  # entries per lane per deep round: -1 auto, 0 -> 4, 1 -> 8
-    _lib.check(_lib.lib().bnmc_gpu_table_set_walk_cap(cache.handle, -1, -1, int(os.environ["BNMC_DEEP"])))
+if os.environ.get("BNMC_DEEP") or os.environ.get("BNMC_WCAP") or os.environ.get("BNMC_WBUD"):
+    # walk cap / budget / entries per lane per deep round (-1: library default)
+    _lib.check(_lib.lib().bnmc_gpu_table_set_walk_cap(
+        cache.handle, int(os.environ.get("BNMC_WCAP", -1)), int(os.environ.get("BNMC_WBUD", -1)),
+        int(os.environ.get("BNMC_DEEP", -1))))
 if os.environ.get("BNMC_ENUM_MAX"):
     _lib.check(_lib.lib().bnmc_gpu_table_set_walk_params(cache.handle, int(os.environ["BNMC_ENUM_MAX"]), -1))
 tws = [int(x) for x in os.environ.get("TW", "0").split(",")]
