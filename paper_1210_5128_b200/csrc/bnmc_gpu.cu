@@ -759,7 +759,7 @@ void launch_walk(bnmc_table* t, const WalkArgs& A, int C, int team_warps = 0,
   int tw = team_warps;
   if (tw == 0)
     tw = C <= sms ? 32 : (C <= 4 * sms ? 8 : (C <= 8 * sms ? 4 : (C <= 16 * sms ? 2 : 1)));
-  const int cta = std::max(kWalkThreads, 32 * tw);
+  const int cta = tw == 1 ? kWalkThreads1 : std::max(kWalkThreads, 32 * tw);
   const int per = cta / (32 * tw);
   const unsigned grid = static_cast<unsigned>((C + per - 1) / per);
   static const bool no_spec = [] {
@@ -780,7 +780,7 @@ void launch_walk(bnmc_table* t, const WalkArgs& A, int C, int team_warps = 0,
   const bool deep = t->walk_deep < 0 ? t->S > kDeepRowEntries : t->walk_deep == 1;
   if (A.recheck) {  // debug_recheck variants (results are identical for every team size)
     const int rtw = tw >= 16 ? 32 : (tw >= 8 ? 8 : 1);
-    const int rcta = std::max(kWalkThreads, 32 * rtw);
+    const int rcta = rtw == 1 ? kWalkThreads1 : std::max(kWalkThreads, 32 * rtw);
     const int rper = rcta / (32 * rtw);
     const unsigned rgrid = static_cast<unsigned>((C + rper - 1) / rper);
     if (rtw == 32) walk_chain_kernel<32, 8, true><<<rgrid, rcta, 0, st>>>(A);

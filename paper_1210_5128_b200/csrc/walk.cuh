@@ -42,6 +42,10 @@ namespace bnmc_dev {
 #define BNMC_WALK_ROUND_INLINE __forceinline__
 #endif
 constexpr int kWalkThreads = 256;
+#ifndef BNMC_WALK_CTA1
+#define BNMC_WALK_CTA1 256
+#endif
+constexpr int kWalkThreads1 = BNMC_WALK_CTA1;  // CTA size of one-warp chains (TW = 1)
 constexpr int kWalkWarps = kWalkThreads / 32;
 #ifndef BNMC_WALK_UNROLL
 #define BNMC_WALK_UNROLL 4
@@ -723,7 +727,7 @@ __device__ __forceinline__ void tracker_offer_warp(uint64_t* tm, double* tt, uin
 // Barrier over the TW warps of one team (a team runs one chain).
 template <int TW>
 __device__ __forceinline__ void team_sync(int team) {
-  constexpr int kCta = TW * 32 > kWalkThreads ? TW * 32 : kWalkThreads;
+  constexpr int kCta = TW == 1 ? kWalkThreads1 : (TW * 32 > kWalkThreads ? TW * 32 : kWalkThreads);
   if constexpr (TW == 1) {
     __syncwarp();
   } else if constexpr (TW * 32 == kCta) {
@@ -830,7 +834,7 @@ __device__ __noinline__ void draw_proposal_batch(TeamState& S, const FastDiv* di
 
 template <int TW>
 __host__ __device__ constexpr int walk_cta_threads() {
-  return TW * 32 > kWalkThreads ? TW * 32 : kWalkThreads;
+  return TW == 1 ? kWalkThreads1 : (TW * 32 > kWalkThreads ? TW * 32 : kWalkThreads);
 }
 
 // TW warps per chain, max(256, 32 TW) / (32 TW) chains per CTA. TW >= 8 gives
