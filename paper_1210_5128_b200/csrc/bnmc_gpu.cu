@@ -1019,6 +1019,9 @@ void walk_launch(bnmc_table* t, const uint64_t* seeds, int C, const bnmc_chain_p
   A.final_score = t->d_fs.p;
   A.accepted = t->d_acc.p;
   A.recheck = params->debug_recheck != 0;
+  // test hook (tests/test_gpu_headline.py): the sequential draw path that
+  // next_below rejections take, forced for every batch
+  A.seq_draws = env_u64("BNMC_SEQ_DRAWS", 0) != 0;
   // Chain blocks: with page-locked result buffers and many chains the chains
   // run as kBlocks launches alternating over two streams, and each block's
   // results are copied to the host while the next block computes (its CTAs

@@ -146,6 +146,7 @@ struct WalkArgs {
                                        // [3] first drifted iteration (debug_recheck)
   int* error;
   int recheck;                         // RunConfig::debug_recheck
+  int seq_draws;                       // test hook: draw every proposal batch sequentially
   // score-only (OrderScorer::score for C orders)
   const int* perms;                    // [C][n] or null
   uint64_t* out_masks;                 // [C][n]
@@ -799,14 +800,14 @@ constexpr int kPropBatch = 32;  // iterations whose proposals are drawn together
 // direct indexing of the splitmix64 sequence (rng.hpp:14-45). Exact: when any
 // draw of the batch falls below next_below's rejection threshold, lane 0
 // redraws the batch sequentially with rejection.
-__device__ __noinline__ void draw_proposal_batch(TeamState& S, const FastDiv* div, int lane) {
+__device__ __noinline__ void draw_proposal_batch(TeamState& S, const FastDiv* div, int lane, bool seq) {
   constexpr uint64_t kGamma = 0x9E3779B97F4A7C15ull;
   const uint64_t s0 = S.rng, sa = S.arng;
   const uint64_t x0 = Rng::mix(s0 + kGamma * (uint64_t)(2 * lane + 1));
   const uint64_t x1 = Rng::mix(s0 + kGamma * (uint64_t)(2 * lane + 2));
   const uint64_t xu = Rng::mix(sa + kGamma * (uint64_t)(lane + 1));
   S.qu[lane] = ((double)(xu >> 11) + 0.5) * 0x1.0p-53;
-  if (__all_sync(0xffffffffu, x0 >= div[0].thr && x1 >= div[1].thr)) {
+  if (!seq && __all_sync(0xffffffffu, x0 >= div[0].thr && x1 >= div[1].thr)) {
     const int a = (int)div[0].mod(x0);
     int b = (int)div[1].mod(x1);
     if (b >= a) ++b;
@@ -891,7 +892,7 @@ __global__ void __launch_bounds__(walk_cta_threads<TW>(), TW == 1 ? kWalkMinBloc
     // one iteration per lane. next_below's rejection (probability ~n/2^64) is
     // detected exactly; such a batch is redrawn in sequence by lane 0.
     if (!BNMC_FRESH && twarp == 0 && ((t - 1) & (kPropBatch - 1)) == 0)
-      draw_proposal_batch(S, s_div, lane);
+      draw_proposal_batch(S, s_div, lane, A.seq_draws != 0);
     if (ttid == 0) {
       int a = 0, b = n - 1;
       if (!BNMC_FRESH) {

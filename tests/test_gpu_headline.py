@@ -175,3 +175,27 @@ def test_pipelined_chain_blocks_equal_single_launch(cfg4):
     for ci in (0, 4095, 4096, 8191, 12288, 16383):  # both sides of every block edge
         r = ref_chain(rc, n, cfg.max_parents, 40, int(seeds[ci]), pri)
         assert_chain_equal(pinned.result(ci), r, f"chain {ci}")
+
+
+def test_sequential_proposal_draws_equal_batched(cfg4, monkeypatch):
+    """draw_proposal_batch's sequential path (taken when a next_below draw is
+    rejected, probability ~n/2^64 per draw) forced for every batch
+    (BNMC_SEQ_DRAWS=1) gives the same chains as the batched path, and both
+    equal the reference for a sampled chain."""
+    data, pri, cfg, cache = cfg4
+    c = P.RunConfig(max_parents=cfg.max_parents, iterations=100, team_warps=1, scan_mode=2,
+                    memory_cap_bytes=cfg.memory_cap_bytes)
+    seeds = np.arange(1, 65, dtype=np.uint64)
+    batched = P.run_chains_batch(cache, pri, seeds, c, P.api.ChainBatch.allocate(64, 100, data.n,
+                                                                                 c.track_top, False))
+    monkeypatch.setenv("BNMC_SEQ_DRAWS", "1")
+    seq = P.run_chains_batch(cache, pri, seeds, c, P.api.ChainBatch.allocate(64, 100, data.n,
+                                                                             c.track_top, False))
+    for f in ("trace_proposed", "trace_accepted", "trace_best", "final_order", "tracker_masks",
+              "tracker_totals"):
+        np.testing.assert_array_equal(np.asarray(getattr(batched, f)).view(np.uint8),
+                                      np.asarray(getattr(seq, f)).view(np.uint8), err_msg=f)
+    if ref.available():
+        rc = ref_cache_of(cache, cfg)
+        assert_chain_equal(seq.result(37), ref_chain(rc, data.n, cfg.max_parents, 100, 38, pri),
+                           "sequential draws, seed 38")
