@@ -1194,18 +1194,47 @@ __global__ void __launch_bounds__(1024, 1) walk_spec_kernel(WalkArgs A) {
   unsigned long long pairs = 0;
   uint64_t t = 0;  // iterations committed so far (0 = initial order not yet scored)
   while (t <= A.iters) {
-    // ---- proposals of this round (thread 0): positions and accept draws
-    if (tid == 0) {
+    // ---- proposals of this round (warp 0, lane i for slot i): positions and
+    // accept draws by direct indexing of the splitmix64 streams (k-th draw =
+    // mix(state + k*gamma)); a next_below rejection anywhere in the round
+    // (probability ~n/2^64) sends the round to lane 0's sequential draws
+    if (warp == 0) {
+      constexpr uint64_t kGamma = 0x9E3779B97F4A7C15ull;
       const int d = t == 0 ? 1 : (int)min((uint64_t)kSpecD, A.iters - t + 1);
-      Rng pr{s_rng}, ar{s_arng};
-      for (int i = 0; i < d; ++i) {
-        SpecSlot& S = s_sl[i];
+      const uint64_t s0 = s_rng, sa = s_arng;
+      const bool mine = lane < d;
+      uint64_t x0 = 0, x1 = 0;
+      if (mine && t > 0) {
+        x0 = Rng::mix(s0 + kGamma * (uint64_t)(2 * lane + 1));
+        x1 = Rng::mix(s0 + kGamma * (uint64_t)(2 * lane + 2));
+      }
+      const bool ok = __all_sync(0xffffffffu, !mine || t == 0 || (x0 >= s_div[0].thr && x1 >= s_div[1].thr));
+      if (ok && mine) {
+        SpecSlot& S = s_sl[lane];
         if (t == 0) {
           S.a = 0;
           S.b = n - 1;
           S.thr = 0.0;
+          S.rng_after = s0;
+          S.arng_after = sa;
         } else {
-          int a = (int)pr.next_below(s_div[0]);  // propose_swap, sampler.cpp:43-52
+          const int a = (int)s_div[0].mod(x0);  // propose_swap, sampler.cpp:43-52
+          int b = (int)s_div[1].mod(x1);
+          if (b >= a) ++b;
+          S.a = a;
+          S.b = b;
+          const uint64_t xu = Rng::mix(sa + kGamma * (uint64_t)(lane + 1));
+          // host glibc log10(u) with host thresholds (the device stream still advances)
+          S.thr = A.thr ? A.thr[(uint64_t)c * (A.iters + 1) + t + lane] : ((double)(xu >> 11) + 0.5) * 0x1.0p-53;
+          S.rng_after = s0 + kGamma * (uint64_t)(2 * lane + 2);
+          S.arng_after = sa + kGamma * (uint64_t)(lane + 1);
+        }
+        S.amb = 0;
+      } else if (!ok && lane == 0) {
+        Rng pr{s0}, ar{sa};
+        for (int i = 0; i < d; ++i) {
+          SpecSlot& S = s_sl[i];
+          int a = (int)pr.next_below(s_div[0]);
           int b = (int)pr.next_below(s_div[1]);
           if (b >= a) ++b;
           S.a = a;
@@ -1213,16 +1242,16 @@ __global__ void __launch_bounds__(1024, 1) walk_spec_kernel(WalkArgs A) {
           const uint64_t it = t + i;
           if (A.thr) {
             S.thr = A.thr[(uint64_t)c * (A.iters + 1) + it];
-            ar.next_u64();  // keep the device stream in step (unused with host thresholds)
+            ar.next_u64();
           } else {
-            S.thr = ar.next_unit_open();  // u; its log10 only if needed (mh_accept_dev)
+            S.thr = ar.next_unit_open();
           }
+          S.rng_after = pr.s;
+          S.arng_after = ar.s;
+          S.amb = 0;
         }
-        S.rng_after = pr.s;
-        S.arng_after = ar.s;
-        S.amb = 0;
       }
-      s_d = d;
+      if (lane == 0) s_d = d;
     }
     __syncthreads();
     const int d = s_d;
